@@ -1,0 +1,173 @@
+/*
+ * fdpp.h — C ABI of the B200-native FlashDecoding++ hot paths
+ * (libfdpp.so, built from paper_2311_01282_b200/csrc for sm_100a).
+ *
+ * Plain pointers and sizes only: every device pointer is caller-owned CUDA
+ * device memory, `stream` is a cudaStream_t passed as void*, and every entry
+ * point returns an fdpp_status (0 = ok).  Calls are stream-ordered and hold
+ * no global state beyond a mutex-guarded TMA descriptor cache, so they are
+ * safe from several host threads on distinct streams and capturable into
+ * CUDA graphs.  Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/flatdecode/<file>:<line>).
+ */
+#ifndef FDPP_H_
+#define FDPP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status */
+typedef enum {
+    FDPP_OK = 0,
+    FDPP_ERR_SHAPE = 1,       /* -> ShapeError (matrix.py:16)            */
+    FDPP_ERR_VALUE = 2,       /* -> ValueError (bad p / scale / mode ...) */
+    FDPP_ERR_CUDA = 3,        /* -> RuntimeError (launch / driver error)  */
+    FDPP_ERR_UNSUPPORTED = 4, /* -> ValueError (dtype / head dim / align) */
+    FDPP_ERR_WORKSPACE = 5    /* -> ValueError (workspace too small)      */
+} fdpp_status;
+
+typedef enum { FDPP_F16 = 0, FDPP_BF16 = 1, FDPP_F32 = 2 } fdpp_dtype;
+
+/* Last error message of the calling thread ("" if none). */
+const char *fdpp_last_error(void);
+/* ABI version (major*100 + minor). */
+int fdpp_version(void);
+/* Streaming-multiprocessor count of the current device (148 on B200), or -1. */
+int fdpp_sm_count(void);
+
+/* ------------------------------------------------- subsystem 1: attention */
+typedef enum { FDPP_ATTN_ASYNC = 0, FDPP_ATTN_SYNC = 1 } fdpp_attn_mode;
+
+/* Split-KV decode/prefill attention over a [B, Hkv, L, D] cache.  Query head
+ * h uses kv head h / (Hq/Hkv); every query row of one (b, kv-head) sees the
+ * same K/V (the reference's "M rows share one K/V", attention.py:77-86).
+ * Semantic chunking is the reference's chunk_bounds(L, p) (softmax.py:103-110);
+ * each chunk is further divided into `splits_per_chunk` CTAs whose partials
+ * are combined in fixed order (bitwise-reproducible reruns). */
+typedef struct fdpp_attn_params {
+    const void *q;            /* [B, Hq, D] (strides below), dtype           */
+    const void *k, *v;        /* [B, Hkv, L, D], key rows contiguous (stride D) */
+    void *o;                  /* [B, Hq, D] output, dtype                     */
+    int32_t dtype;            /* fdpp_dtype                                  */
+    int32_t B, Hq, Hkv, L, D; /* D in {8,16,32,64,128,256} (f32: <= 128)      */
+    int64_t q_stride_b, q_stride_h;   /* elements                           */
+    int64_t kv_stride_b, kv_stride_h; /* elements (K and V share strides)    */
+    int64_t o_stride_b, o_stride_h;   /* elements                           */
+    float scale;              /* logit scale (AttentionConfig.scale)         */
+    float phi, a, b;          /* ScalingCalibration (softmax.py:175-197)      */
+    int32_t p;                /* semantic chunk count (AttentionConfig.p)     */
+    int32_t splits_per_chunk; /* CTAs per chunk; 0 = auto (fill 148 SMs)      */
+    int32_t mode;             /* fdpp_attn_mode                              */
+    uint8_t *row_flags;       /* [B, Hq] out (async): 1 = row recomputed      */
+    int32_t *viol_index;      /* optional [B, Hq, p] out: first violating key
+                                 of each chunk, or -1 (attention.py:217-238)   */
+    int32_t *rows_recomputed; /* optional device counter, incremented         */
+    float *chunk_num;         /* optional [B, Hq, p, D] out: async chunk states
+                                 num_j (zeroed for a violating chunk)          */
+    float *chunk_den;         /* optional [B, Hq, p] out: async chunk den_j    */
+    void *workspace;          /* zero-filled before first use; kernels leave
+                                 its counters zeroed on exit                   */
+    size_t workspace_bytes;
+} fdpp_attn_params;
+
+/* Bytes of workspace `fdpp_attn_decode` needs for these params. */
+fdpp_status fdpp_attn_workspace_size(const fdpp_attn_params *p, size_t *bytes);
+
+/* The semantic chunk count and CTAs per chunk the call will use (resolves
+ * p = 0 / splits_per_chunk = 0 "auto"); AttnStats arithmetic uses this p. */
+fdpp_status fdpp_attn_plan(const fdpp_attn_params *p, int32_t *chunks, int32_t *splits_per_chunk);
+
+/* Replaces batch_decode_attention(Q, K, V, cfg, mode) for mode in
+ * {"async", "sync"} (attention.py:308-321) and the per-row recompute of
+ * _batch_async (attention.py:266-286).  ASYNC: unified-phi partials, fused
+ * band check, fixed-order chunk join, then the synchronized recompute of
+ * flagged rows (always launched; CTAs of unflagged rows exit at once).
+ * SYNC: FlashDecoding split-KV with the Eq. (2) max-rescaled join. */
+fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream);
+
+/* ------------------------------------------- subsystem 2: flat GEMM family */
+typedef enum { FDPP_IMPL_A = 0, FDPP_IMPL_B = 1, FDPP_IMPL_C = 2 } fdpp_impl;
+
+/* C[M,N] = A[M,K] · W[N,K]^T (+ R[M,N]); W is the reference's B[K,N]
+ * prepacked to [N, ldw] (fdpp_prepack_weight).  fp32 accumulation,
+ * fixed-order (deterministic) reductions, dtype in {F16, BF16}. */
+typedef struct fdpp_gemm_params {
+    const void *a; int64_t lda;   /* [M, K] activations                       */
+    const void *w; int64_t ldw;   /* [N, K] prepacked weight, ldw % 8 == 0     */
+    void *c; int64_t ldc;         /* [M, N] output                            */
+    const void *r; int64_t ldr;   /* optional residual added in the epilogue
+                                     (may alias c)                             */
+    int32_t M, N, K;
+    int32_t dtype;                /* FDPP_F16 or FDPP_BF16                     */
+    int32_t block_x;              /* ImplB/C token-tile rows; 0 = auto         */
+    int32_t splits;               /* split-K factor; 0 = auto                  */
+    int32_t stages;               /* smem ring depth; 0 = auto (1 = single
+                                     buffer, 2 = the paper's double buffer)     */
+    void *workspace;              /* split-K partials + tile counters (zeroed
+                                     before first use, left zeroed)            */
+    size_t workspace_bytes;
+} fdpp_gemm_params;
+
+/* Transpose the reference's row-major B[K,N] into W[N, ldw] (zero pad K..ldw). */
+fdpp_status fdpp_prepack_weight(const void *b_kn, void *w_nk, int32_t K, int32_t N,
+                                int64_t ldw, int32_t dtype, void *stream);
+fdpp_status fdpp_gemm_workspace_size(int32_t impl, const fdpp_gemm_params *p, size_t *bytes);
+
+/* ImplA (dispatch.py:73-90): CUDA-core GEMV for M <= 8, weights streamed
+ * once for all rows (the reference re-streams B per row). */
+fdpp_status fdpp_impl_a_gemv(const fdpp_gemm_params *p, void *stream);
+/* ImplB (dispatch.py:140-145 / flatgemm.py:215-242): swap-AB tcgen05 flat
+ * GEMM — weight rows on the MMA M axis (128), tokens on the MMA N axis
+ * (16..64, TMA zero-fills the padding), TMA/mbarrier ring, N-split grid with
+ * deterministic split-K. */
+fdpp_status fdpp_impl_b_flat(const fdpp_gemm_params *p, void *stream);
+/* ImplC (dispatch.py:117-137): conventional tcgen05 GEMM, tokens on the MMA
+ * M axis (128-row tiles). */
+fdpp_status fdpp_impl_c_gemm(const fdpp_gemm_params *p, void *stream);
+/* run_kernel(choice, a, b) (dispatch.py:155-156). */
+fdpp_status fdpp_run_kernel(int32_t impl, const fdpp_gemm_params *p, void *stream);
+
+/* ------------------------------------------ subsystem 3: heuristic dispatch */
+/* dispatch(m, n, k, table) on one entry (dispatch.py:189-197): 0=A,1=B,2=C. */
+int32_t fdpp_dispatch_choose(int32_t m, int32_t m1, int32_t m2);
+/* _first_sustained (dispatch.py:248-265); returns index or -1 for None. */
+int32_t fdpp_first_sustained(const double *costs_new, const double *costs_old,
+                             int32_t n, int32_t start);
+/* Decision flow of profile_shape (dispatch.py:326-338) on measured medians. */
+fdpp_status fdpp_profile_decide(const int32_t *m_sweep, const double *med_a,
+                                const double *med_b, const double *med_c, int32_t n,
+                                int32_t *m1, int32_t *m2);
+/* chunk_bounds(n, p) (softmax.py:103-110) into bounds[p+1]. */
+fdpp_status fdpp_chunk_bounds(int64_t n, int32_t p, int64_t *bounds);
+
+/* --------------------------- decode-step glue (caller of the hot path, §8f) */
+/* out = x * rsqrt(mean(x^2) + eps) * w, rows of length dim. */
+fdpp_status fdpp_rmsnorm(const void *x, const void *w, void *out, int32_t rows, int32_t dim,
+                         float eps, int32_t dtype, void *stream);
+/* Rotary embedding on the q/k parts of a fused [B, (Hq+2*Hkv)*D] qkv row at
+ * position pos[b], writing q to q_out [B, Hq, D] and appending k/v to the
+ * caches at row pos[b] ([B, Hkv, Lmax, D], strides in elements). */
+fdpp_status fdpp_rope_append(const void *qkv, void *q_out, void *k_cache, void *v_cache,
+                             const int32_t *pos, int32_t B, int32_t Hq, int32_t Hkv,
+                             int32_t D, int64_t cache_stride_b, int64_t cache_stride_h,
+                             float theta, int32_t dtype, void *stream);
+/* out[r, j] = silu(gu[r, j]) * gu[r, F + j] for a fused [rows, 2F] gate/up. */
+fdpp_status fdpp_silu_mul(const void *gu, void *out, int32_t rows, int32_t F, int32_t dtype,
+                          void *stream);
+/* out[b, :] = table[ids[b], :]. */
+fdpp_status fdpp_embed(const int32_t *ids, const void *table, void *out, int32_t B, int32_t dim,
+                       int32_t dtype, void *stream);
+/* ids[r] = argmax_j logits[r, j] (lowest index on ties). */
+fdpp_status fdpp_argmax(const void *logits, int32_t *ids, int32_t rows, int32_t vocab,
+                        int32_t dtype, void *stream);
+/* pos[b] += 1 for b < B (advances the decode position on device). */
+fdpp_status fdpp_advance_positions(int32_t *pos, int32_t B, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FDPP_H_ */

@@ -1,0 +1,587 @@
+// Subsystem 1 — split-KV decode/prefill attention on sm_100a.
+//
+// attn_split_kernel<ASYNC=true>  FlashDecoding++ asynchronized softmax
+//   (attention.py:167-199 + :217-238 + :266-286): every CTA owns one sub-range
+//   of one semantic chunk (chunk_bounds(L, p), softmax.py:103-110) for all the
+//   query rows of its (batch, kv-head) row group.  K/V tiles stream through a
+//   4-stage shared-memory ring filled by the TMA bulk engine (cp.async.bulk,
+//   one producer warp); four consumer warps read 16-B vectors from shared
+//   memory, reduce dot products with warp shuffles, apply the unified scale
+//   phi, check the open band (a, b) per logit, and accumulate e^(x - phi) and
+//   e^(x - phi)·v in fp32 with no max and no rescale.  The last CTA of the row
+//   group (atomic ticket) joins all partials in fixed chunk/sub-range order,
+//   applies the reference's "non-finite chunk state is a violation" rule and
+//   writes O plus the per-row recompute flag.
+//
+// attn_split_kernel<ASYNC=false> FlashDecoding synchronized softmax
+//   (attention.py:91-162): per-lane online max/rescale, Eq. (2) merge across
+//   lanes, warps and sub-ranges in fixed order.  It serves mode="sync" and the
+//   recompute of flagged rows: with `only_flagged`, row groups without a
+//   flagged row exit before touching memory, so the launch can always be made
+//   (graph-capturable, no host round trip).
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace fdpp {
+
+constexpr int ATT_CONSUMERS = 4;                       // consumer warps
+constexpr int ATT_THREADS = (ATT_CONSUMERS + 1) * 32;  // + 1 producer warp
+constexpr int ATT_STAGES = 4;
+constexpr int ATT_MAX_P = 1024;                        // semantic chunks per row
+
+struct AttnArgs {
+    const void *q, *k, *v;
+    void *o;
+    int B, Hq, Hkv, L, G, n_rg;  // G = Hq / Hkv, n_rg = row groups per kv head
+    int64_t q_sb, q_sh, kv_sb, kv_sh, o_sb, o_sh;
+    float scale, phi, a, b;
+    int p, nsub;
+    uint8_t *row_flags;
+    int32_t *viol_index;
+    int32_t *rows_recomputed;
+    float *chunk_num, *chunk_den;
+    bool only_flagged;
+    // workspace
+    float *ws_num;  // [B*Hq][p*nsub][D]
+    float *ws_den;  // [B*Hq][p*nsub]
+    float *ws_m;    // [B*Hq][p*nsub]
+    int *ws_viol;   // [B*Hq][p*nsub]
+    int *counters;  // [B*Hkv*n_rg]
+};
+
+template <typename T, int D>
+struct AttnGeom {
+    static constexpr int RB = D * (int)sizeof(T);         // bytes per key row
+    static constexpr int VEC = 16 / (int)sizeof(T);       // elements per 16-B lane chunk
+    static constexpr int LPK = RB / 16;                   // lanes per key
+    static constexpr int KPI = 32 / LPK;                  // keys per warp iteration
+    static constexpr int TK_RAW = 8192 / RB;
+    static constexpr int TK = TK_RAW < 16 ? 16 : (TK_RAW > 256 ? 256 : TK_RAW);  // keys per stage
+    static constexpr int STAGE_BYTES = 2 * TK * RB;       // K tile + V tile
+    static_assert(LPK >= 1 && LPK <= 32 && (32 % LPK) == 0, "head dim");
+    static_assert(TK % (ATT_CONSUMERS * KPI) == 0, "tile");
+};
+
+__device__ __forceinline__ int chunk_lo(int L, int p, int j) { return (L / p) * j; }
+__device__ __forceinline__ int chunk_hi(int L, int p, int j) { return j == p - 1 ? L : (L / p) * (j + 1); }
+
+template <typename T, int VEC>
+__device__ __forceinline__ void load_vec(const T *src, float (&out)[VEC]) {
+    int4 raw = *reinterpret_cast<const int4 *>(src);
+    if constexpr (sizeof(T) == 4) {
+        out[0] = __int_as_float(raw.x);
+        out[1] = __int_as_float(raw.y);
+        out[2] = __int_as_float(raw.z);
+        out[3] = __int_as_float(raw.w);
+    } else {
+        uint32_t w[4] = {(uint32_t)raw.x, (uint32_t)raw.y, (uint32_t)raw.z, (uint32_t)raw.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float2 f = Elem<T>::to_f2(w[i]);
+            out[2 * i] = f.x;
+            out[2 * i + 1] = f.y;
+        }
+    }
+}
+
+__device__ __forceinline__ float safe_scale(float m, float mref) {
+    return m == -INFINITY ? 0.f : __expf(m - mref);
+}
+
+template <typename T, int D, int GT, bool ASYNC>
+__global__ void __launch_bounds__(ATT_THREADS)
+attn_split_kernel(const AttnArgs args) {
+    using Gm = AttnGeom<T, D>;
+    constexpr int VEC = Gm::VEC, LPK = Gm::LPK, KPI = Gm::KPI, TK = Gm::TK, RB = Gm::RB;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + ATT_STAGES * Gm::STAGE_BYTES);
+    uint64_t *empty = full + ATT_STAGES;
+    float *red = reinterpret_cast<float *>(empty + ATT_STAGES);  // [CONSUMERS][GT][D+2]
+    // join scratch aliases the K/V ring (free once every tile has been consumed)
+    float *s_cden = reinterpret_cast<float *>(smem);
+    int *s_cviol = reinterpret_cast<int *>(smem) + ATT_MAX_P;
+    int *s_unrep = reinterpret_cast<int *>(smem) + 2 * ATT_MAX_P;
+    static_assert(ATT_STAGES * Gm::STAGE_BYTES >= 3 * ATT_MAX_P * 4, "join scratch");
+    __shared__ int s_last, s_any_flag;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int P = args.p * args.nsub;
+    const int cta = blockIdx.x;               // (chunk, sub) index in [0, P)
+    const int j = cta / args.nsub, sub = cta % args.nsub;
+    const int rg = blockIdx.y % args.n_rg, kvh = blockIdx.y / args.n_rg, b = blockIdx.z;
+    const int g0 = rg * GT;
+    const int gcount = min(GT, args.G - g0);
+    const int h0 = kvh * args.G + g0;         // first query head of this row group
+
+    if (!ASYNC && args.only_flagged) {        // recompute launch: skip clean row groups
+        int any = 0;
+        for (int g = 0; g < gcount; ++g) any |= args.row_flags[(int64_t)b * args.Hq + h0 + g];
+        if (!any) return;
+    }
+
+    const int lo_j = chunk_lo(args.L, args.p, j), hi_j = chunk_hi(args.L, args.p, j);
+    const int per = (hi_j - lo_j + args.nsub - 1) / args.nsub;
+    const int k_begin = min(hi_j, lo_j + sub * per);
+    const int k_end = min(hi_j, k_begin + per);
+    const int nkeys = k_end - k_begin;
+    const int ntiles = (nkeys + TK - 1) / TK;
+
+    const T *kbase = static_cast<const T *>(args.k) + (int64_t)b * args.kv_sb + (int64_t)kvh * args.kv_sh;
+    const T *vbase = static_cast<const T *>(args.v) + (int64_t)b * args.kv_sb + (int64_t)kvh * args.kv_sh;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ATT_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], ATT_CONSUMERS);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int row0 = b * args.Hq + h0;        // global row index of g = 0
+
+    if (warp == ATT_CONSUMERS) {
+        // ------------------------------------------------ producer warp
+        if (lane == 0) {
+            for (int t = 0; t < ntiles; ++t) {
+                const int s = t % ATT_STAGES;
+                const uint32_t ph = (t / ATT_STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                const int key0 = k_begin + t * TK;
+                const int n = min(TK, k_end - key0);
+                const uint32_t bytes = (uint32_t)n * RB;
+                uint8_t *dk = smem + s * Gm::STAGE_BYTES;
+                uint8_t *dv = dk + TK * RB;
+                mbar_arrive_expect_tx(&full[s], 2 * bytes);
+                bulk_g2s(dk, kbase + (int64_t)key0 * D, bytes, &full[s], kEvictFirst);
+                bulk_g2s(dv, vbase + (int64_t)key0 * D, bytes, &full[s], kEvictFirst);
+            }
+        }
+    } else {
+        // ------------------------------------------------ consumer warps
+        const int c = lane % LPK;          // 16-B chunk of the head dim owned by this lane
+        const int kg = lane / LPK;         // key slot inside a warp iteration
+        float q[GT][VEC];
+#pragma unroll
+        for (int g = 0; g < GT; ++g) {
+            if (g < gcount) {
+                const T *qp = static_cast<const T *>(args.q) + (int64_t)b * args.q_sb +
+                              (int64_t)(h0 + g) * args.q_sh + c * VEC;
+                load_vec<T, VEC>(qp, q[g]);
+            } else {
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) q[g][v] = 0.f;
+            }
+        }
+        float num[GT][VEC], den[GT], mx[GT];
+        int viol[GT];
+#pragma unroll
+        for (int g = 0; g < GT; ++g) {
+            den[g] = 0.f;
+            mx[g] = -INFINITY;
+            viol[g] = INT_MAX;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) num[g][v] = 0.f;
+        }
+        const float scale = args.scale, phi = args.phi, ba = args.a, bb = args.b;
+
+        for (int t = 0; t < ntiles; ++t) {
+            const int s = t % ATT_STAGES;
+            const uint32_t ph = (t / ATT_STAGES) & 1;
+            mbar_wait(&full[s], ph);
+            const int key0 = k_begin + t * TK;
+            const int n = min(TK, k_end - key0);
+            const T *sk = reinterpret_cast<const T *>(smem + s * Gm::STAGE_BYTES);
+            const T *sv = sk + TK * D;
+#pragma unroll 2
+            for (int kk0 = warp * KPI; kk0 < n; kk0 += ATT_CONSUMERS * KPI) {
+                const int kk = kk0 + kg;
+                const bool valid = kk < n;
+                float kf[VEC];
+                load_vec<T, VEC>(sk + (valid ? kk : 0) * D + c * VEC, kf);
+                float dot[GT];
+#pragma unroll
+                for (int g = 0; g < GT; ++g) {
+                    float sacc = 0.f;
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) sacc = fmaf(q[g][v], kf[v], sacc);
+#pragma unroll
+                    for (int o = LPK / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+                    dot[g] = sacc;
+                }
+                float vf[VEC];
+                load_vec<T, VEC>(sv + (valid ? kk : 0) * D + c * VEC, vf);
+#pragma unroll
+                for (int g = 0; g < GT; ++g) {
+                    const float x = dot[g] * scale;       // logit, reference order: scale * acc
+                    float e;
+                    if constexpr (ASYNC) {
+                        const float ti = x - phi;
+                        const bool bad = (ti <= ba) || (ti >= bb);
+                        if (valid && bad) viol[g] = min(viol[g], key0 + kk);
+                        e = (valid && !bad) ? __expf(ti) : 0.f;
+                    } else {
+                        if (valid && x > mx[g]) {         // online max: rescale running state
+                            const float f = safe_scale(mx[g], x);
+                            den[g] *= f;
+#pragma unroll
+                            for (int v = 0; v < VEC; ++v) num[g][v] *= f;
+                            mx[g] = x;
+                        }
+                        e = valid ? __expf(x - mx[g]) : 0.f;
+                    }
+                    den[g] += e;
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) num[g][v] = fmaf(e, vf[v], num[g][v]);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+
+        // ---- reduce across the key slots of the warp (lanes with equal c), fixed butterfly
+#pragma unroll
+        for (int g = 0; g < GT; ++g) {
+#pragma unroll
+            for (int o = LPK; o < 32; o <<= 1) {
+                if constexpr (ASYNC) {
+                    den[g] += __shfl_xor_sync(0xffffffffu, den[g], o);
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) num[g][v] += __shfl_xor_sync(0xffffffffu, num[g][v], o);
+                    viol[g] = min(viol[g], __shfl_xor_sync(0xffffffffu, viol[g], o));
+                } else {
+                    const float m2 = __shfl_xor_sync(0xffffffffu, mx[g], o);
+                    const float l2 = __shfl_xor_sync(0xffffffffu, den[g], o);
+                    const float mm = fmaxf(mx[g], m2);
+                    const float f1 = safe_scale(mx[g], mm), f2 = safe_scale(m2, mm);
+                    den[g] = den[g] * f1 + l2 * f2;
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) {
+                        const float a2 = __shfl_xor_sync(0xffffffffu, num[g][v], o);
+                        num[g][v] = num[g][v] * f1 + a2 * f2;
+                    }
+                    mx[g] = mm;
+                }
+            }
+        }
+        // ---- per-warp partials to shared memory: red[w][g][0..D) = num, [D] = den, [D+1] = m/viol
+        if (kg == 0) {
+#pragma unroll
+            for (int g = 0; g < GT; ++g) {
+                float *r = red + (warp * GT + g) * (D + 2);
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) r[c * VEC + v] = num[g][v];
+                if (c == 0) {
+                    r[D] = den[g];
+                    r[D + 1] = ASYNC ? __int_as_float(viol[g]) : mx[g];
+                }
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- merge the consumer warps in fixed order and write this CTA's partial
+    for (int idx = threadIdx.x; idx < gcount * (D + 2); idx += ATT_THREADS) {
+        const int g = idx / (D + 2), e = idx % (D + 2);
+        const int64_t slot = (int64_t)(row0 + g) * P + cta;
+        if (ASYNC) {
+            if (e < D) {
+                float s = 0.f;
+                for (int w = 0; w < ATT_CONSUMERS; ++w) s += red[(w * GT + g) * (D + 2) + e];
+                args.ws_num[slot * D + e] = s;
+            } else if (e == D) {
+                float s = 0.f;
+                for (int w = 0; w < ATT_CONSUMERS; ++w) s += red[(w * GT + g) * (D + 2) + D];
+                args.ws_den[slot] = s;
+            } else {
+                int vm = INT_MAX;
+                for (int w = 0; w < ATT_CONSUMERS; ++w)
+                    vm = min(vm, __float_as_int(red[(w * GT + g) * (D + 2) + D + 1]));
+                args.ws_viol[slot] = vm;
+            }
+        } else {
+            float mm = -INFINITY;
+            for (int w = 0; w < ATT_CONSUMERS; ++w) mm = fmaxf(mm, red[(w * GT + g) * (D + 2) + D + 1]);
+            float s = 0.f;
+            for (int w = 0; w < ATT_CONSUMERS; ++w) {
+                const float *r = red + (w * GT + g) * (D + 2);
+                s += r[e < D ? e : D] * safe_scale(r[D + 1], mm);
+            }
+            if (e < D) args.ws_num[slot * D + e] = s;
+            else if (e == D) args.ws_den[slot] = s;
+            else args.ws_m[slot] = mm;
+        }
+    }
+
+    // ---- last CTA of the row group joins all partials (fixed order)
+    __threadfence();
+    __syncthreads();
+    const int counter = (b * args.Hkv + kvh) * args.n_rg + rg;
+    if (threadIdx.x == 0) {
+        const int ticket = atomicAdd(&args.counters[counter], 1);
+        s_last = (ticket == P - 1);
+        if (s_last) args.counters[counter] = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+
+    for (int g = 0; g < gcount; ++g) {
+        const int64_t row = row0 + g;
+        const int64_t base = row * P;
+        if (!ASYNC && args.only_flagged && !args.row_flags[row]) continue;
+        T *op = static_cast<T *>(args.o) + (int64_t)b * args.o_sb + (int64_t)(h0 + g) * args.o_sh;
+        if (ASYNC) {
+            // pass 1: chunk exp-sums and first violation per chunk
+            for (int jj = threadIdx.x; jj < args.p; jj += ATT_THREADS) {
+                float cd = 0.f;
+                int vm = INT_MAX;
+                for (int s = 0; s < args.nsub; ++s) {
+                    cd += ld_cg_f32(&args.ws_den[base + jj * args.nsub + s]);
+                    vm = min(vm, __ldcg(&args.ws_viol[base + jj * args.nsub + s]));
+                }
+                s_cden[jj] = cd;
+                s_cviol[jj] = vm;
+                s_unrep[jj] = !isfinite(cd);
+            }
+            if (threadIdx.x == 0) s_any_flag = 0;
+            __syncthreads();
+            // pass 2: chunk numerators (non-finite chunk state => violation, attention.py:230-237)
+            float tot[(D + ATT_THREADS - 1) / ATT_THREADS];
+            int nd = 0;
+            for (int d = threadIdx.x; d < D; d += ATT_THREADS, ++nd) {
+                float acc = 0.f;
+                for (int jj = 0; jj < args.p; ++jj) {
+                    float cn = 0.f;
+                    for (int s = 0; s < args.nsub; ++s)
+                        cn += ld_cg_f32(&args.ws_num[(base + jj * args.nsub + s) * D + d]);
+                    if (!isfinite(cn)) s_unrep[jj] = 1;  // benign race: all writers store 1
+                    if (args.chunk_num)  // chunk state; a violating chunk is zeroed (attention.py:191-194)
+                        args.chunk_num[(row * args.p + jj) * D + d] = s_cviol[jj] == INT_MAX ? cn : 0.f;
+                    acc += cn;
+                }
+                tot[nd] = acc;
+            }
+            __syncthreads();
+            // pass 3: chunk verdicts, row flag
+            for (int jj = threadIdx.x; jj < args.p; jj += ATT_THREADS) {
+                int v = s_cviol[jj];
+                if (v == INT_MAX) v = s_unrep[jj] ? chunk_lo(args.L, args.p, jj) : -1;
+                if (args.viol_index) args.viol_index[row * args.p + jj] = v;
+                if (args.chunk_den) args.chunk_den[row * args.p + jj] = s_cviol[jj] == INT_MAX ? s_cden[jj] : 0.f;
+                if (v >= 0) s_any_flag = 1;
+            }
+            __syncthreads();
+            const bool flagged = s_any_flag != 0;
+            if (threadIdx.x == 0) {
+                args.row_flags[row] = flagged ? 1 : 0;
+                if (flagged && args.rows_recomputed) atomicAdd(args.rows_recomputed, 1);
+            }
+            if (!flagged) {
+                float dsum = 0.f;
+                for (int jj = 0; jj < args.p; ++jj) dsum += s_cden[jj];  // chunk order
+                nd = 0;
+                for (int d = threadIdx.x; d < D; d += ATT_THREADS, ++nd)
+                    op[d] = Elem<T>::from_f(tot[nd] / dsum);
+            }
+            __syncthreads();
+        } else {
+            // Eq. (2) join over all (chunk, sub-range) partials in index order
+            float mrow = -INFINITY;
+            for (int i = 0; i < P; ++i) mrow = fmaxf(mrow, ld_cg_f32(&args.ws_m[base + i]));
+            float l = 0.f;
+            for (int i = 0; i < P; ++i)
+                l += ld_cg_f32(&args.ws_den[base + i]) * safe_scale(ld_cg_f32(&args.ws_m[base + i]), mrow);
+            for (int d = threadIdx.x; d < D; d += ATT_THREADS) {
+                float acc = 0.f;
+                for (int i = 0; i < P; ++i)
+                    acc += ld_cg_f32(&args.ws_num[(base + i) * D + d]) *
+                           safe_scale(ld_cg_f32(&args.ws_m[base + i]), mrow);
+                op[d] = Elem<T>::from_f(acc / l);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------- host
+struct AttnLayout {
+    int G, GT, n_rg, p, nsub, P;
+    size_t off_num, off_den, off_m, off_viol, off_cnt, total;
+};
+
+static int pick_gt(int G) { return G >= 8 ? 8 : G >= 4 ? 4 : G >= 2 ? 2 : 1; }
+
+static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
+    FDPP_REQUIRE(p != nullptr, FDPP_ERR_VALUE, "null params");
+    FDPP_REQUIRE(p->B >= 1 && p->Hq >= 1 && p->Hkv >= 1 && p->L >= 1, FDPP_ERR_SHAPE,
+                 "attention dims must be >= 1 (K/V cache must hold at least one row)");
+    FDPP_REQUIRE(p->Hq % p->Hkv == 0, FDPP_ERR_SHAPE, "Hq %% Hkv != 0");
+    lay->G = p->Hq / p->Hkv;
+    lay->GT = pick_gt(lay->G);
+    lay->n_rg = (lay->G + lay->GT - 1) / lay->GT;
+    const int groups = p->B * p->Hkv * lay->n_rg;
+    const int sms = sm_count() > 0 ? sm_count() : 148;
+    if (p->p > 0) {
+        FDPP_REQUIRE(p->p <= p->L, FDPP_ERR_VALUE, "partition count must be in [1, %d], got %d",
+                     p->L, p->p);
+        FDPP_REQUIRE(p->p <= ATT_MAX_P, FDPP_ERR_VALUE, "partition count above %d", ATT_MAX_P);
+        lay->p = p->p;
+    } else {
+        // auto: enough chunks to give ~2 waves of CTAs, >= 128 keys per chunk
+        int want = (2 * sms + groups - 1) / groups;
+        int maxp = p->L / 128 > 0 ? p->L / 128 : 1;
+        lay->p = want < 1 ? 1 : (want > maxp ? maxp : want);
+        if (lay->p > ATT_MAX_P) lay->p = ATT_MAX_P;
+    }
+    if (p->splits_per_chunk > 0) {
+        lay->nsub = p->splits_per_chunk;
+    } else {
+        const int per_chunk = p->L / lay->p;
+        int want = (2 * sms + groups * lay->p - 1) / (groups * lay->p);
+        int maxs = per_chunk / 64 > 0 ? per_chunk / 64 : 1;  // >= 64 keys per CTA
+        lay->nsub = want < 1 ? 1 : (want > maxs ? maxs : want);
+    }
+    lay->P = lay->p * lay->nsub;
+    const size_t rows = (size_t)p->B * p->Hq;
+    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+    size_t off = 0;
+    lay->off_cnt = off;  off += al((size_t)groups * sizeof(int));
+    lay->off_num = off;  off += al(rows * lay->P * p->D * sizeof(float));
+    lay->off_den = off;  off += al(rows * lay->P * sizeof(float));
+    lay->off_m = off;    off += al(rows * lay->P * sizeof(float));
+    lay->off_viol = off; off += al(rows * lay->P * sizeof(int));
+    lay->total = off;
+    return FDPP_OK;
+}
+
+template <typename T, int D, int GT, bool ASYNC>
+static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st) {
+    using Gm = AttnGeom<T, D>;
+    const int smem = ATT_STAGES * Gm::STAGE_BYTES + 2 * ATT_STAGES * 8 +
+                     ATT_CONSUMERS * GT * (D + 2) * (int)sizeof(float);
+    auto kern = attn_split_kernel<T, D, GT, ASYNC>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn)");
+        attr = true;
+    }
+    dim3 grid(grid_x, a.Hkv * a.n_rg, a.B);
+    kern<<<grid, ATT_THREADS, smem, st>>>(a);
+    FDPP_CHECK_LAUNCH("attn_split_kernel");
+    return FDPP_OK;
+}
+
+template <typename T, int D, bool ASYNC>
+static fdpp_status by_gt(const AttnArgs &a, int gt, int gx, cudaStream_t st) {
+    switch (gt) {
+        case 1: return launch_attn<T, D, 1, ASYNC>(a, gx, st);
+        case 2: return launch_attn<T, D, 2, ASYNC>(a, gx, st);
+        case 4: return launch_attn<T, D, 4, ASYNC>(a, gx, st);
+        default: return launch_attn<T, D, 8, ASYNC>(a, gx, st);
+    }
+}
+
+template <typename T, bool ASYNC>
+static fdpp_status by_d(const AttnArgs &a, int D, int gt, int gx, cudaStream_t st) {
+    switch (D) {
+        case 8: return by_gt<T, 8, ASYNC>(a, gt, gx, st);
+        case 16: return by_gt<T, 16, ASYNC>(a, gt, gx, st);
+        case 32: return by_gt<T, 32, ASYNC>(a, gt, gx, st);
+        case 64: return by_gt<T, 64, ASYNC>(a, gt, gx, st);
+        case 128: return by_gt<T, 128, ASYNC>(a, gt, gx, st);
+        case 256:
+            if constexpr (sizeof(T) == 2) return by_gt<T, 256, ASYNC>(a, gt, gx, st);
+            else break;
+        case 4:
+            if constexpr (sizeof(T) == 4) return by_gt<T, 4, ASYNC>(a, gt, gx, st);
+            else break;
+        default: break;
+    }
+    set_error("unsupported head dim %d for this dtype (pad D to a power of two >= 16 bytes)", D);
+    return FDPP_ERR_UNSUPPORTED;
+}
+
+template <bool ASYNC>
+static fdpp_status by_dtype(const AttnArgs &a, int dtype, int D, int gt, int gx, cudaStream_t st) {
+    switch (dtype) {
+        case FDPP_F16: return by_d<__half, ASYNC>(a, D, gt, gx, st);
+        case FDPP_BF16: return by_d<__nv_bfloat16, ASYNC>(a, D, gt, gx, st);
+        case FDPP_F32: return by_d<float, ASYNC>(a, D, gt, gx, st);
+        default: set_error("bad dtype %d", dtype); return FDPP_ERR_UNSUPPORTED;
+    }
+}
+
+}  // namespace fdpp
+
+using namespace fdpp;
+
+extern "C" fdpp_status fdpp_attn_workspace_size(const fdpp_attn_params *p, size_t *bytes) {
+    FDPP_REQUIRE(bytes != nullptr, FDPP_ERR_VALUE, "null bytes");
+    AttnLayout lay;
+    fdpp_status s = layout_for(p, &lay);
+    if (s != FDPP_OK) return s;
+    *bytes = lay.total;
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_attn_plan(const fdpp_attn_params *p, int32_t *chunks,
+                                      int32_t *splits_per_chunk) {
+    FDPP_REQUIRE(chunks && splits_per_chunk, FDPP_ERR_VALUE, "null output");
+    AttnLayout lay;
+    fdpp_status s = layout_for(p, &lay);
+    if (s != FDPP_OK) return s;
+    *chunks = lay.p;
+    *splits_per_chunk = lay.nsub;
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream) {
+    AttnLayout lay;
+    fdpp_status s = layout_for(p, &lay);
+    if (s != FDPP_OK) return s;
+    FDPP_REQUIRE(p->q && p->k && p->v && p->o, FDPP_ERR_VALUE, "null attention operand");
+    FDPP_REQUIRE(p->mode == FDPP_ATTN_ASYNC || p->mode == FDPP_ATTN_SYNC, FDPP_ERR_VALUE,
+                 "mode must be async or sync");
+    FDPP_REQUIRE(p->scale > 0.f, FDPP_ERR_VALUE, "scale must be > 0");
+    FDPP_REQUIRE(p->mode != FDPP_ATTN_ASYNC || p->row_flags, FDPP_ERR_VALUE,
+                 "async mode needs row_flags");
+    FDPP_REQUIRE(p->workspace && p->workspace_bytes >= lay.total, FDPP_ERR_WORKSPACE,
+                 "attention workspace too small: need %zu bytes", lay.total);
+    const int esz = p->dtype == FDPP_F32 ? 4 : 2;
+    FDPP_REQUIRE((reinterpret_cast<uintptr_t>(p->k) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(p->v) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(p->q) & 15) == 0 &&
+                     ((p->kv_stride_b * esz) & 15) == 0 && ((p->kv_stride_h * esz) & 15) == 0 &&
+                     ((p->q_stride_b * esz) & 15) == 0 && ((p->q_stride_h * esz) & 15) == 0,
+                 FDPP_ERR_UNSUPPORTED, "Q/K/V must be 16-byte aligned per row/head");
+    char *ws = static_cast<char *>(p->workspace);
+    AttnArgs a{};
+    a.q = p->q; a.k = p->k; a.v = p->v; a.o = p->o;
+    a.B = p->B; a.Hq = p->Hq; a.Hkv = p->Hkv; a.L = p->L; a.G = lay.G; a.n_rg = lay.n_rg;
+    a.q_sb = p->q_stride_b; a.q_sh = p->q_stride_h;
+    a.kv_sb = p->kv_stride_b; a.kv_sh = p->kv_stride_h;
+    a.o_sb = p->o_stride_b; a.o_sh = p->o_stride_h;
+    a.scale = p->scale; a.phi = p->phi; a.a = p->a; a.b = p->b;
+    a.p = lay.p; a.nsub = lay.nsub;
+    a.row_flags = p->row_flags; a.viol_index = p->viol_index; a.rows_recomputed = p->rows_recomputed;
+    a.chunk_num = p->chunk_num; a.chunk_den = p->chunk_den;
+    a.ws_num = reinterpret_cast<float *>(ws + lay.off_num);
+    a.ws_den = reinterpret_cast<float *>(ws + lay.off_den);
+    a.ws_m = reinterpret_cast<float *>(ws + lay.off_m);
+    a.ws_viol = reinterpret_cast<int *>(ws + lay.off_viol);
+    a.counters = reinterpret_cast<int *>(ws + lay.off_cnt);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (p->mode == FDPP_ATTN_SYNC) {
+        a.only_flagged = false;
+        return by_dtype<false>(a, p->dtype, p->D, lay.GT, lay.P, st);
+    }
+    a.only_flagged = false;
+    s = by_dtype<true>(a, p->dtype, p->D, lay.GT, lay.P, st);
+    if (s != FDPP_OK) return s;
+    // synchronized recompute of flagged rows (attention.py:283-285), always launched
+    a.only_flagged = true;
+    return by_dtype<false>(a, p->dtype, p->D, lay.GT, lay.P, st);
+}

@@ -1,0 +1,190 @@
+// Decode-step glue around the hot path: the small
+// bandwidth-trivial kernels a real Llama decode step needs between the
+// dispatched GEMMs and the attention op.  All fp32 math, fixed-order
+// reductions, one CTA (or warp) per row.
+#include "common.cuh"
+
+namespace fdpp {
+
+template <typename T>
+__global__ void rmsnorm_kernel(const T *__restrict__ x, const T *__restrict__ w, T *__restrict__ out,
+                               int dim, float eps) {
+    const int row = blockIdx.x;
+    const T *xr = x + (int64_t)row * dim;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
+        const float v = Elem<T>::to_f(xr[i]);
+        ss = fmaf(v, v, ss);
+    }
+    __shared__ float red[32];
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float inv = rsqrtf(red[0] / dim + eps);
+    for (int i = threadIdx.x; i < dim; i += blockDim.x)
+        out[(int64_t)row * dim + i] = Elem<T>::from_f(Elem<T>::to_f(xr[i]) * inv * Elem<T>::to_f(w[i]));
+}
+
+// one block per batch row; thread i handles rotary pair (i, i + D/2) of one head
+template <typename T>
+__global__ void rope_append_kernel(const T *__restrict__ qkv, T *__restrict__ q_out, T *__restrict__ kc,
+                                   T *__restrict__ vc, const int32_t *__restrict__ pos, int Hq, int Hkv,
+                                   int D, int64_t csb, int64_t csh, float theta) {
+    const int b = blockIdx.x;
+    const int half = D / 2;
+    const int width = (Hq + 2 * Hkv) * D;
+    const T *row = qkv + (int64_t)b * width;
+    const int p = pos[b];
+    for (int idx = threadIdx.x; idx < (Hq + Hkv) * half; idx += blockDim.x) {
+        const int h = idx / half, i = idx % half;
+        const float inv_freq = __powf(theta, -2.f * i / D);
+        float sn, cs;
+        __sincosf(p * inv_freq, &sn, &cs);
+        const T *src = row + h * D;  // q heads then k heads are contiguous in the fused row
+        const float x0 = Elem<T>::to_f(src[i]), x1 = Elem<T>::to_f(src[i + half]);
+        const T r0 = Elem<T>::from_f(x0 * cs - x1 * sn), r1 = Elem<T>::from_f(x1 * cs + x0 * sn);
+        if (h < Hq) {
+            T *dst = q_out + ((int64_t)b * Hq + h) * D;
+            dst[i] = r0;
+            dst[i + half] = r1;
+        } else {
+            T *dst = kc + (int64_t)b * csb + (int64_t)(h - Hq) * csh + (int64_t)p * D;
+            dst[i] = r0;
+            dst[i + half] = r1;
+        }
+    }
+    const T *vsrc = row + (Hq + Hkv) * D;
+    for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x) {
+        const int h = idx / D, i = idx % D;
+        vc[(int64_t)b * csb + (int64_t)h * csh + (int64_t)p * D + i] = vsrc[h * D + i];
+    }
+}
+
+template <typename T>
+__global__ void silu_mul_kernel(const T *__restrict__ gu, T *__restrict__ out, int F) {
+    const int r = blockIdx.y;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
+        const float g = Elem<T>::to_f(gu[(int64_t)r * 2 * F + j]);
+        const float u = Elem<T>::to_f(gu[(int64_t)r * 2 * F + F + j]);
+        out[(int64_t)r * F + j] = Elem<T>::from_f(g / (1.f + __expf(-g)) * u);
+    }
+}
+
+template <typename T>
+__global__ void embed_kernel(const int32_t *__restrict__ ids, const T *__restrict__ table,
+                             T *__restrict__ out, int dim) {
+    const int b = blockIdx.x;
+    const int64_t id = ids[b];
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) out[(int64_t)b * dim + i] = table[id * dim + i];
+}
+
+template <typename T>
+__global__ void argmax_kernel(const T *__restrict__ logits, int32_t *__restrict__ ids, int vocab) {
+    const int r = blockIdx.x;
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int j = threadIdx.x; j < vocab; j += blockDim.x) {
+        const float v = Elem<T>::to_f(logits[(int64_t)r * vocab + j]);
+        if (v > best || (v == best && j < bi)) { best = v; bi = j; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float v2 = __shfl_xor_sync(0xffffffffu, best, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (v2 > best || (v2 == best && i2 < bi)) { best = v2; bi = i2; }
+    }
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+            if (sv[w] > best || (sv[w] == best && si[w] < bi)) { best = sv[w]; bi = si[w]; }
+        ids[r] = bi;
+    }
+}
+
+__global__ void advance_kernel(int32_t *pos, int B) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < B) pos[b] += 1;
+}
+
+}  // namespace fdpp
+
+using namespace fdpp;
+
+#define FDPP_DT_SWITCH(dtype, ...)                                       \
+    switch (dtype) {                                                     \
+        case FDPP_F16: { using T = __half; __VA_ARGS__; break; }         \
+        case FDPP_BF16: { using T = __nv_bfloat16; __VA_ARGS__; break; } \
+        case FDPP_F32: { using T = float; __VA_ARGS__; break; }          \
+        default: set_error("bad dtype %d", dtype); return FDPP_ERR_UNSUPPORTED; \
+    }
+
+extern "C" fdpp_status fdpp_rmsnorm(const void *x, const void *w, void *out, int32_t rows,
+                                    int32_t dim, float eps, int32_t dtype, void *stream) {
+    FDPP_REQUIRE(rows >= 1 && dim >= 1, FDPP_ERR_SHAPE, "rmsnorm dims");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FDPP_DT_SWITCH(dtype, rmsnorm_kernel<T><<<rows, 512, 0, st>>>(
+                              static_cast<const T *>(x), static_cast<const T *>(w),
+                              static_cast<T *>(out), dim, eps));
+    FDPP_CHECK_LAUNCH("rmsnorm_kernel");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_rope_append(const void *qkv, void *q_out, void *k_cache, void *v_cache,
+                                        const int32_t *pos, int32_t B, int32_t Hq, int32_t Hkv,
+                                        int32_t D, int64_t csb, int64_t csh, float theta,
+                                        int32_t dtype, void *stream) {
+    FDPP_REQUIRE(B >= 1 && Hq >= 1 && Hkv >= 1 && D >= 2 && D % 2 == 0, FDPP_ERR_SHAPE, "rope dims");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FDPP_DT_SWITCH(dtype, rope_append_kernel<T><<<B, 512, 0, st>>>(
+                              static_cast<const T *>(qkv), static_cast<T *>(q_out),
+                              static_cast<T *>(k_cache), static_cast<T *>(v_cache), pos, Hq, Hkv,
+                              D, csb, csh, theta));
+    FDPP_CHECK_LAUNCH("rope_append_kernel");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_silu_mul(const void *gu, void *out, int32_t rows, int32_t F,
+                                     int32_t dtype, void *stream) {
+    FDPP_REQUIRE(rows >= 1 && F >= 1, FDPP_ERR_SHAPE, "silu_mul dims");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    dim3 grid(ceil_div(F, 256) < 16 ? ceil_div(F, 256) : 16, rows);
+    FDPP_DT_SWITCH(dtype, silu_mul_kernel<T><<<grid, 256, 0, st>>>(static_cast<const T *>(gu),
+                                                                   static_cast<T *>(out), F));
+    FDPP_CHECK_LAUNCH("silu_mul_kernel");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_embed(const int32_t *ids, const void *table, void *out, int32_t B,
+                                  int32_t dim, int32_t dtype, void *stream) {
+    FDPP_REQUIRE(B >= 1 && dim >= 1, FDPP_ERR_SHAPE, "embed dims");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FDPP_DT_SWITCH(dtype, embed_kernel<T><<<B, 256, 0, st>>>(ids, static_cast<const T *>(table),
+                                                             static_cast<T *>(out), dim));
+    FDPP_CHECK_LAUNCH("embed_kernel");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_argmax(const void *logits, int32_t *ids, int32_t rows, int32_t vocab,
+                                   int32_t dtype, void *stream) {
+    FDPP_REQUIRE(rows >= 1 && vocab >= 1, FDPP_ERR_SHAPE, "argmax dims");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    FDPP_DT_SWITCH(dtype, argmax_kernel<T><<<rows, 1024, 0, st>>>(static_cast<const T *>(logits),
+                                                                  ids, vocab));
+    FDPP_CHECK_LAUNCH("argmax_kernel");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_advance_positions(int32_t *pos, int32_t B, void *stream) {
+    FDPP_REQUIRE(B >= 1, FDPP_ERR_SHAPE, "B");
+    advance_kernel<<<ceil_div(B, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(pos, B);
+    FDPP_CHECK_LAUNCH("advance_kernel");
+    return FDPP_OK;
+}

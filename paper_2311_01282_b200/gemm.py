@@ -1,0 +1,163 @@
+"""Device GEMM plumbing shared by flatgemm.py and dispatch.py.
+
+C[M,N] = A[M,K] · B[K,N] with B prepacked once into W[N, ldw] (K-major, the
+layout both the GEMV and the tcgen05 TMA tiles stream), fp16/bf16 storage,
+fp32 accumulation.  Reference-API calls with numpy f32 operands are rounded
+to fp16 on the device (the precision the B200 path computes in; north_star:
+"fp16/bf16 with fp32 accumulation", 2e-3 relative bar).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _lib, workspace
+from .matrix import ShapeError
+
+IMPL_A, IMPL_B, IMPL_C = _lib.IMPL_A, _lib.IMPL_B, _lib.IMPL_C
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class PackedWeight:
+    """A weight prepacked for libfdpp: ``w`` is [N, ldw] (ldw = K rounded up to
+    8, zero padded), the transpose of the reference's row-major B[K, N]."""
+
+    __slots__ = ("w", "K", "N", "ldw")
+
+    def __init__(self, w, K: int, N: int):
+        self.w, self.K, self.N, self.ldw = w, int(K), int(N), int(w.stride(0))
+
+    @property
+    def dtype(self):
+        return self.w.dtype
+
+    @classmethod
+    def from_nk(cls, w_nk):
+        """Wrap an [N, K] (already K-major) weight, e.g. an nn.Linear weight."""
+        torch = _torch()
+        N, K = w_nk.shape
+        if K % 8 or w_nk.stride(1) != 1 or w_nk.stride(0) % 8:
+            w2 = torch.zeros((N, (K + 7) // 8 * 8), dtype=w_nk.dtype, device=w_nk.device)
+            w2[:, :K] = w_nk
+            w_nk = w2
+        return cls(w_nk, K, N)
+
+
+def pack_weight(b_kn, dtype=None, stream=None) -> PackedWeight:
+    """Prepack the reference's B[K, N] on the device (fdpp_prepack_weight)."""
+    torch = _torch()
+    _lib.require_cuda()
+    if not isinstance(b_kn, torch.Tensor):
+        b_kn = torch.from_numpy(np.ascontiguousarray(b_kn, dtype=np.float32)).cuda()
+    if dtype is None:
+        dtype = b_kn.dtype if b_kn.dtype in (torch.float16, torch.bfloat16) else torch.float16
+    b = b_kn.to(device="cuda", dtype=dtype).contiguous()
+    if b.dim() != 2:
+        raise ShapeError("weight must be 2-D [K, N]")
+    K, N = b.shape
+    ldw = (K + 7) // 8 * 8
+    w = torch.empty((N, ldw), dtype=dtype, device=b.device)
+    _lib.check(_lib.load().fdpp_prepack_weight(b.data_ptr(), w.data_ptr(), K, N, ldw,
+                                               _lib.dtype_code(dtype), _lib.stream_handle(stream)),
+               "prepack_weight")
+    return PackedWeight(w, K, N)
+
+
+_cache_lock = threading.Lock()
+_pack_cache: dict = {}
+
+
+def as_packed(b, dtype=None) -> PackedWeight:
+    """PackedWeight for b (cached by tensor identity + version for CUDA tensors)."""
+    torch = _torch()
+    if isinstance(b, PackedWeight):
+        return b
+    if isinstance(b, torch.Tensor) and b.is_cuda:
+        key = (b.data_ptr(), tuple(b.shape), tuple(b.stride()), b.dtype, b._version, dtype)
+        with _cache_lock:
+            hit = _pack_cache.get(key)
+        if hit is not None:
+            return hit
+        pw = pack_weight(b, dtype)
+        with _cache_lock:
+            if len(_pack_cache) > 256:
+                _pack_cache.clear()
+            _pack_cache[key] = pw
+        return pw
+    return pack_weight(b, dtype)
+
+
+def as_activation(a, dtype):
+    """Device [M, K] activation with K padded to a multiple of 8."""
+    torch = _torch()
+    if not isinstance(a, torch.Tensor):
+        a = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+    a = a.to(device="cuda", dtype=dtype)
+    if a.dim() != 2:
+        raise ShapeError("activation must be 2-D [M, K]")
+    M, K = a.shape
+    if K % 8 or a.stride(1) != 1 or a.stride(0) % 8 or a.data_ptr() % 16:
+        a2 = torch.zeros((M, (K + 7) // 8 * 8), dtype=dtype, device=a.device)
+        a2[:, :K] = a
+        a = a2
+    return a
+
+
+def gemm_params(a, pw: PackedWeight, out, residual=None, block_x=0, splits=0, stages=0):
+    prm = _lib.GemmParams()
+    prm.a, prm.lda = a.data_ptr(), a.stride(0)
+    prm.w, prm.ldw = pw.w.data_ptr(), pw.ldw
+    prm.c, prm.ldc = out.data_ptr(), out.stride(0)
+    if residual is not None:
+        prm.r, prm.ldr = residual.data_ptr(), residual.stride(0)
+    prm.M, prm.N, prm.K = a.shape[0], pw.N, pw.ldw  # zero-padded K contributes exactly 0
+    prm.dtype = _lib.dtype_code(a.dtype)
+    prm.block_x, prm.splits, prm.stages = int(block_x), int(splits), int(stages)
+    return prm
+
+
+def run(impl: int, a, pw: PackedWeight, *, out=None, residual=None, block_x=0, splits=0,
+        stages=0, stream=None, ws_tag="gemm"):
+    """Launch ImplA/B/C on device operands; returns out [M, N]."""
+    torch = _torch()
+    if a.shape[1] != pw.ldw:
+        raise ShapeError(f"inner dims disagree: {tuple(a.shape)} x [K={pw.K}, N={pw.N}]")
+    if a.dtype != pw.dtype:
+        raise ValueError(f"activation dtype {a.dtype} != weight dtype {pw.dtype}")
+    if out is None:
+        out = torch.empty((a.shape[0], pw.N), dtype=a.dtype, device=a.device)
+    prm = gemm_params(a, pw, out, residual, block_x, splits, stages)
+    lib = _lib.load()
+    need = ctypes.c_size_t()
+    _lib.check(lib.fdpp_gemm_workspace_size(impl, ctypes.byref(prm), ctypes.byref(need)), "gemm")
+    if need.value:
+        ws = workspace.get(need.value, a.device, tag=ws_tag)
+        prm.workspace, prm.workspace_bytes = ws.data_ptr(), ws.numel()
+    _lib.check(lib.fdpp_run_kernel(impl, ctypes.byref(prm), _lib.stream_handle(stream)),
+               ("ImplA", "ImplB", "ImplC")[impl])
+    return out
+
+
+def reference_call(impl: int, a, b, **kw):
+    """Reference-signature call: a [M,K], b [K,N] (numpy f32 or tensors)."""
+    torch = _torch()
+    _lib.require_cuda()
+    if a.shape[1] != (b.K if isinstance(b, PackedWeight) else b.shape[0]):
+        raise ShapeError(f"inner dims disagree: {tuple(a.shape)} x {tuple(getattr(b, 'shape', (b.K, b.N)))}")
+    was_numpy = not isinstance(a, torch.Tensor)
+    dtype = torch.float16
+    if isinstance(a, torch.Tensor) and a.dtype in (torch.float16, torch.bfloat16):
+        dtype = a.dtype
+    pw = as_packed(b, dtype)
+    A = as_activation(a, dtype)
+    if A.shape[1] != pw.ldw:
+        raise ShapeError("inner dims disagree")
+    c = run(impl, A, pw, **kw)
+    return c.float().cpu().numpy() if was_numpy else c

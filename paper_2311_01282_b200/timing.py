@@ -1,0 +1,51 @@
+"""Device-side timing for the profiler and bench (reference: flatdecode/timing.py).
+
+``median_mad`` keeps the reference's definition (timing.py:8-13).
+``measure`` replaces the wall clock (timing.py:16-25) with CUDA events on the
+launching stream, synchronised on both sides, and flushes L2 before each
+timed rep so a kernel never reports cache bandwidth as HBM bandwidth.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+_FLUSH = {}
+
+
+def median_mad(samples):
+    s = np.asarray(samples, dtype=np.float64)
+    med = float(np.median(s))
+    mad = float(np.median(np.abs(s - med)))
+    return med, mad
+
+
+def l2_flush(device=None, nbytes: int = 256 << 20):
+    """Overwrite a buffer twice the 126 MB L2 so the next kernel starts cold."""
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    buf = _FLUSH.get(dev.index)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        _FLUSH[dev.index] = buf
+    buf.zero_()
+
+
+def measure(fn, reps: int, warmup: int = 2, flush_l2: bool = True):
+    """Seconds per call of fn(), one CUDA-event pair per rep, after warmup."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    out = []
+    stream = torch.cuda.current_stream()
+    for _ in range(reps):
+        if flush_l2:
+            l2_flush()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        out.append(e0.elapsed_time(e1) * 1e-3)
+    return out

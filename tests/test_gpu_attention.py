@@ -1,0 +1,216 @@
+"""GPU parity of subsystem 1 (async-softmax split-KV attention) through the
+C ABI against the reference's golden vectors and the oracle.
+
+Bars (north_star): outputs within 2e-3 relative (rowwise, metrics.py:19-32),
+recompute-flag sets bit-exact, AttnStats arithmetic exact, reruns bitwise."""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import flatdecode_oracle as O
+from tests.conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3          # north_star bar for fp16/bf16 storage
+TOL_F32 = 2e-5      # fp32 inputs: only summation order differs from the oracle
+
+ATT = np.load(os.path.join(GOLDEN, "attention.npz"))
+
+
+@pytest.fixture(scope="module")
+def fd():
+    import paper_2311_01282_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+def _case(i, fd):
+    pre = f"c{i}_"
+    meta = ATT[pre + "meta"]
+    calib = fd.ScalingCalibration(phi=float(meta[2]), a=float(meta[3]), b=float(meta[4]),
+                                  coverage=1.0)
+    cfg = fd.AttentionConfig(p=int(meta[0]), scale=float(meta[1]), calib=calib)
+    return ATT[pre + "Q"], ATT[pre + "K"], ATT[pre + "V"], cfg, pre
+
+
+@pytest.mark.parametrize("i", range(int(ATT["n_cases"])))
+def test_golden_async_sync(i, fd):
+    Q, K, V, cfg, pre = _case(i, fd)
+    out, st = fd.batch_decode_attention(Q, K, V, cfg, "async")
+    assert fd.rel_error_rowwise(out, ATT[pre + "out_async"]) <= TOL_F32
+    assert np.array_equal(st.row_mask.numpy(), ATT[pre + "redo"])
+    assert [st.rows_recomputed, st.rescale_ops, st.max_ops] == ATT[pre + "stats_async"].tolist()
+    out, st = fd.batch_decode_attention(Q, K, V, cfg, "sync")
+    assert fd.rel_error_rowwise(out, ATT[pre + "out_sync"]) <= TOL_F32
+    assert [st.rows_recomputed, st.rescale_ops, st.max_ops] == ATT[pre + "stats_sync"].tolist()
+    out, _ = fd.batch_decode_attention(Q, K, V, cfg, "reference")
+    assert fd.rel_error_rowwise(out, ATT[pre + "out_ref"]) <= 1e-6
+
+
+@pytest.mark.parametrize("i", range(int(ATT["n_cases"])))
+def test_golden_chunk_states(i, fd):
+    Q, K, V, cfg, pre = _case(i, fd)
+    num, den, viol = fd.async_partials(Q, K, V, cfg)
+    assert np.array_equal(viol, ATT[pre + "viol"])          # first violating key, bit-exact
+    gden = ATT[pre + "den"].astype(np.float32)
+    ok = np.isfinite(gden)
+    assert np.allclose(den[ok], gden[ok], rtol=1e-5, atol=1e-30)
+    gnum = ATT[pre + "num"].astype(np.float32)
+    M, p, d = gnum.shape
+    fin = np.isfinite(gnum).all(axis=2).reshape(-1)
+    if fin.any():
+        a = num.reshape(M * p, d)[fin]
+        g = gnum.reshape(M * p, d)[fin]
+        if np.abs(g).max() > 0:
+            assert fd.rel_error_rowwise(a, g) <= 1e-5
+
+
+def test_worked_example_state(fd):
+    # test_attention.py:95-143: phi=6, band (-3, 3), K = I
+    calib = fd.ScalingCalibration(phi=6.0, a=-3.0, b=3.0, coverage=1.0)
+    cfg = fd.AttentionConfig(p=2, scale=1.0, calib=calib)
+    K = np.eye(4, dtype=np.float32)
+    V = np.random.default_rng(7).standard_normal((4, 4)).astype(np.float32)
+    q = np.array([4.0, 5.0, 9.5, 7.0], np.float32)
+    st = fd.async_chunk_state(q, K, V, 2, 4, cfg)
+    assert st.overflow_index == 2 and st.den == 0.0 and not st.num.any()
+    o, rec = fd.decode_attention_async(q, K, V, cfg)
+    assert rec
+    assert np.array_equal(o, fd.decode_attention_sync(q, K, V, cfg))
+
+
+def _qkv(torch, B, Hq, Hkv, L, D, seed, dtype):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q = torch.randn((B, Hq, D), generator=g, device="cuda").to(dtype)
+    k = torch.randn((B, Hkv, L, D), generator=g, device="cuda").to(dtype)
+    v = torch.randn((B, Hkv, L, D), generator=g, device="cuda").to(dtype)
+    return q, k, v
+
+
+def _oracle_batched(q, k, v, p, scale, calib):
+    """Run the oracle per (b, kv-head) with the G query rows of that group."""
+    B, Hq, D = q.shape
+    Hkv = k.shape[1]
+    G = Hq // Hkv
+    qn, kn, vn = (t.float().cpu().numpy() for t in (q, k, v))
+    out = np.zeros((B, Hq, D), np.float32)
+    redo = np.zeros((B, Hq), bool)
+    clear = np.ones((B, Hq), bool)
+    for b in range(B):
+        for h in range(Hkv):
+            Qg = qn[b, h * G:(h + 1) * G]
+            o, _, r = O.batch_decode_attention(Qg, kn[b, h], vn[b, h], p, scale, calib, "async")
+            out[b, h * G:(h + 1) * G] = o
+            redo[b, h * G:(h + 1) * G] = r
+            c, _ = O.row_guard_ok(Qg, kn[b, h], scale, calib)
+            clear[b, h * G:(h + 1) * G] = c
+    return out, redo, clear
+
+
+GOLD_CAL = (-7.775933742523193, -1.0, 16.577659606933594)
+
+
+@pytest.mark.parametrize("dtype_name", ["float16", "bfloat16"])
+def test_config1_llama_mha(fd, torch, dtype_name):
+    # config 1: batch 1, 32 heads x 128, L=1024, N(0,1) inputs, golden calibration
+    dtype = getattr(torch, dtype_name)
+    q, k, v = _qkv(torch, 1, 32, 32, 1024, 128, 0, dtype)
+    calib = fd.ScalingCalibration(*GOLD_CAL, coverage=1.0)
+    cfg = fd.AttentionConfig(p=4, scale=1 / math.sqrt(128), calib=calib)
+    o, st = fd.decode_attention(q, k, v, cfg, "async")
+    oc = O.Calib(*GOLD_CAL)
+    ref, redo, clear = _oracle_batched(q, k, v, 4, cfg.scale, oc)
+    assert clear.all()
+    assert st.rows_recomputed == 0 and not redo.any()
+    assert fd.rel_error_rowwise(o.float().cpu().numpy().reshape(-1, 128), ref.reshape(-1, 128)) <= TOL
+    o2, _ = fd.decode_attention(q, k, v, cfg, "async")
+    assert torch.equal(o, o2)                                   # bitwise rerun
+
+
+def test_mqa_recompute_flags(fd, torch):
+    # config 4 shape family (MQA, G=16) at reduced L: inject rows x12 outside the band
+    B, Hq, Hkv, L, D = 2, 32, 2, 2048, 128
+    q, k, v = _qkv(torch, B, Hq, Hkv, L, D, 1, torch.float16)
+    inject = [(0, 3), (0, 17), (1, 30), (1, 0), (1, 5)]
+    for b, h in inject:
+        q[b, h] = (q[b, h].float() * 12).half()
+    calib = fd.ScalingCalibration(*GOLD_CAL, coverage=1.0)
+    for p, spc in ((4, 0), (7, 3), (1, 1)):
+        cfg = fd.AttentionConfig(p=p, scale=1 / math.sqrt(D), calib=calib, splits_per_chunk=spc)
+        o, st = fd.decode_attention(q, k, v, cfg, "async")
+        ref, redo, clear = _oracle_batched(q, k, v, p, cfg.scale, O.Calib(*GOLD_CAL))
+        assert clear.all()
+        assert np.array_equal(st.row_mask.cpu().numpy(), redo)   # flag set bit-exact
+        assert st.rows_recomputed == len(inject)
+        assert st.rescale_ops == 2 * len(inject) * p
+        assert st.max_ops == len(inject) * (p + 1)
+        assert fd.rel_error_rowwise(o.float().cpu().numpy().reshape(-1, D), ref.reshape(-1, D)) <= TOL
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8, 16])
+def test_gqa_groups_sync_and_async(fd, torch, G):
+    Hkv = 2
+    q, k, v = _qkv(torch, 2, Hkv * G, Hkv, 777, 128, 3 + G, torch.float16)
+    calib = fd.ScalingCalibration(*GOLD_CAL, coverage=1.0)
+    cfg = fd.AttentionConfig(p=3, scale=1 / math.sqrt(128), calib=calib)
+    ref, _, _ = _oracle_batched(q, k, v, 3, cfg.scale, O.Calib(*GOLD_CAL))
+    for mode in ("async", "sync"):
+        o, _ = fd.decode_attention(q, k, v, cfg, mode)
+        assert fd.rel_error_rowwise(o.float().cpu().numpy().reshape(-1, 128), ref.reshape(-1, 128)) <= TOL
+
+
+@pytest.mark.parametrize("inject", [0, 1, 5])
+def test_acceptance_criterion_3(fd, inject):
+    # test_acceptance.py:92-112 through the drop-in API: r rows recomputed, exact count
+    rng = np.random.default_rng(33 + inject)
+    calib = fd.ScalingCalibration(phi=0.0, a=-8.0, b=8.0, coverage=1.0)
+    worst = 0.0
+    for _ in range(25):
+        M, L, d = 8, 64, 16
+        K = rng.standard_normal((L, d), dtype=np.float32)
+        V = rng.standard_normal((L, d), dtype=np.float32)
+        Q = rng.standard_normal((M, d), dtype=np.float32)
+        lg = Q.astype(np.float64) @ K.astype(np.float64).T
+        Q *= (6.0 / np.abs(lg).max(axis=1, keepdims=True)).astype(np.float32)
+        rows = rng.choice(M, size=inject, replace=False)
+        Q[rows] *= 3.0
+        cfg = fd.AttentionConfig(p=4, scale=1.0, calib=calib)
+        out, st = fd.batch_decode_attention(Q, K, V, cfg, "async")
+        assert st.rows_recomputed == inject
+        worst = max(worst, fd.rel_error_rowwise(out, O.attention_reference(Q, K, V, 1.0)))
+    assert worst <= 1e-5
+
+
+def test_adversarial_span_sync(fd):
+    d = 8
+    K = np.eye(d, dtype=np.float32)
+    V = np.random.default_rng(5).standard_normal((d, d)).astype(np.float32)
+    q = np.array([40.0, -40.0, 20.0, -20.0, 0.0, 10.0, -10.0, 30.0], dtype=np.float32)
+    out = fd.decode_attention_sync(q, K, V, fd.AttentionConfig(p=4, scale=1.0))
+    assert fd.rel_error_rowwise(out, O.attention_reference(q[None], K, V, 1.0)[0]) <= 1e-5
+
+
+def test_errors(fd):
+    Q = np.ones((1, 8), np.float32)
+    with pytest.raises(ValueError):
+        fd.batch_decode_attention(Q, np.ones((4, 8), np.float32), np.ones((4, 8), np.float32),
+                                  fd.AttentionConfig(p=2, scale=1.0), "turbo")
+    with pytest.raises(ValueError, match="alibration"):
+        fd.batch_decode_attention(Q, np.ones((4, 8), np.float32), np.ones((4, 8), np.float32),
+                                  fd.AttentionConfig(p=2, scale=1.0), "async")
+    with pytest.raises(fd.ShapeError):
+        fd.batch_decode_attention(np.ones((2, 3), np.float32), np.ones((4, 5), np.float32),
+                                  np.ones((4, 5), np.float32), fd.AttentionConfig(p=1, scale=1.0), "sync")
+    with pytest.raises(ValueError):
+        fd.batch_decode_attention(Q, np.ones((4, 8), np.float32), np.ones((4, 8), np.float32),
+                                  fd.AttentionConfig(p=9, scale=1.0), "sync")
