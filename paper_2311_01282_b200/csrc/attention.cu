@@ -447,7 +447,8 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
     const size_t rows = (size_t)p->B * p->Hq;
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     size_t off = 0;
-    lay->off_cnt = off;  off += al((size_t)groups * sizeof(int));
+    FDPP_REQUIRE(groups <= kWsCounters, FDPP_ERR_SHAPE, "too many (batch, kv-head) groups: %d", groups);
+    lay->off_cnt = off;  off += kWsCounterBytes;
     lay->off_num = off;  off += al(rows * lay->P * p->D * sizeof(float));
     lay->off_den = off;  off += al(rows * lay->P * sizeof(float));
     lay->off_m = off;    off += al(rows * lay->P * sizeof(float));

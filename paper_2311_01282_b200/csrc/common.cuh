@@ -35,6 +35,12 @@ int sm_count();
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+// Every workspace starts with a fixed region of ticket counters that is never
+// used for anything else, so a pooled buffer reused by a differently shaped
+// call can never see partial sums where it expects zeroed counters.
+constexpr int kWsCounters = 16384;
+constexpr size_t kWsCounterBytes = kWsCounters * sizeof(int);
+
 // ------------------------------------------------------------- element types
 template <typename T> struct Elem;
 template <> struct Elem<__half> {

