@@ -57,6 +57,10 @@ typedef struct fdpp_attn_params {
     int64_t q_stride_b, q_stride_h;   /* elements                           */
     int64_t kv_stride_b, kv_stride_h; /* elements (K and V share strides)    */
     int64_t o_stride_b, o_stride_h;   /* elements                           */
+    const int32_t *seq_lens;  /* optional [B] device lengths (<= L): batch row b
+                                 attends to its first seq_lens[b] keys, read at
+                                 run time so one captured graph serves every
+                                 decode step; NULL = L for every row           */
     float scale;              /* logit scale (AttentionConfig.scale)         */
     float phi, a, b;          /* ScalingCalibration (softmax.py:175-197)      */
     int32_t p;                /* semantic chunk count (AttentionConfig.p)     */
@@ -164,8 +168,9 @@ fdpp_status fdpp_embed(const int32_t *ids, const void *table, void *out, int32_t
 /* ids[r] = argmax_j logits[r, j] (lowest index on ties). */
 fdpp_status fdpp_argmax(const void *logits, int32_t *ids, int32_t rows, int32_t vocab,
                         int32_t dtype, void *stream);
-/* pos[b] += 1 for b < B (advances the decode position on device). */
-fdpp_status fdpp_advance_positions(int32_t *pos, int32_t B, void *stream);
+/* pos[b] += 1 and lens[b] = pos[b] + 1 for b < B (advances the decode
+ * position and the attended length on device; lens may be NULL). */
+fdpp_status fdpp_advance_positions(int32_t *pos, int32_t *lens, int32_t B, void *stream);
 
 #ifdef __cplusplus
 }

@@ -29,6 +29,7 @@ class AttnParams(ctypes.Structure):
         ("q_stride_b", c_i64), ("q_stride_h", c_i64),
         ("kv_stride_b", c_i64), ("kv_stride_h", c_i64),
         ("o_stride_b", c_i64), ("o_stride_h", c_i64),
+        ("seq_lens", c_vp),
         ("scale", c_f32), ("phi", c_f32), ("a", c_f32), ("b", c_f32),
         ("p", c_i32), ("splits_per_chunk", c_i32), ("mode", c_i32),
         ("row_flags", c_vp), ("viol_index", c_vp), ("rows_recomputed", c_vp),
@@ -74,7 +75,7 @@ SIGNATURES = {
     "fdpp_silu_mul": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_embed": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_argmax": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
-    "fdpp_advance_positions": (c_i32, [c_vp, c_i32, c_vp]),
+    "fdpp_advance_positions": (c_i32, [c_vp, c_vp, c_i32, c_vp]),
 }
 
 _lib = None

@@ -159,14 +159,16 @@ def _params(q, k, v, o, cfg, mode, L):
 
 
 def decode_attention(q, k_cache, v_cache, cfg: AttentionConfig, mode: str = "async", *,
-                     out=None, L: Optional[int] = None, row_flags=None, viol_index=None,
-                     chunk_num=None, chunk_den=None, stream=None):
+                     out=None, L: Optional[int] = None, seq_lens=None, row_flags=None,
+                     viol_index=None, chunk_num=None, chunk_den=None, counter=None, stream=None):
     """Batched decode attention on CUDA tensors.
 
     q [B, Hq, D]; k_cache / v_cache [B, Hkv, Lmax, D] (key rows contiguous);
-    attends to the first L (default Lmax) keys.  Returns (out [B, Hq, D],
-    AttnStats).  Capturable into CUDA graphs when ``out`` / ``row_flags`` are
-    preallocated (no allocation, no host sync).
+    attends to the first L (default Lmax) keys, or to ``seq_lens[b]`` keys of
+    batch row b when an int32 device tensor is given (read at run time).
+    Returns (out [B, Hq, D], AttnStats).  Capturable into CUDA graphs when
+    ``out`` / ``row_flags`` / ``counter`` are preallocated (no allocation, no
+    host sync).
     """
     torch = _torch()
     if mode not in ("sync", "async"):
@@ -189,8 +191,13 @@ def decode_attention(q, k_cache, v_cache, cfg: AttentionConfig, mode: str = "asy
         out = torch.empty((B, Hq, D), dtype=q.dtype, device=q.device)
     if row_flags is None:
         row_flags = torch.zeros((B, Hq), dtype=torch.uint8, device=q.device)
-    counter = torch.zeros(1, dtype=torch.int32, device=q.device) if mode == "async" else None
+    if counter is None and mode == "async":
+        counter = torch.zeros(1, dtype=torch.int32, device=q.device)
     prm = _params(q, k_cache, v_cache, out, cfg, mode, L)
+    if seq_lens is not None:
+        if seq_lens.dtype != torch.int32 or not seq_lens.is_cuda or seq_lens.numel() < B:
+            raise ValueError("seq_lens must be an int32 CUDA tensor with one entry per batch row")
+        prm.seq_lens = seq_lens.data_ptr()
     prm.row_flags = row_flags.data_ptr()
     prm.viol_index = viol_index.data_ptr() if viol_index is not None else None
     prm.rows_recomputed = counter.data_ptr() if counter is not None else None

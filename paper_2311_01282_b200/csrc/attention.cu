@@ -35,6 +35,7 @@ struct AttnArgs {
     void *o;
     int B, Hq, Hkv, L, G, n_rg;  // G = Hq / Hkv, n_rg = row groups per kv head
     int64_t q_sb, q_sh, kv_sb, kv_sh, o_sb, o_sh;
+    const int32_t *seq_lens;
     float scale, phi, a, b;
     int p, nsub;
     uint8_t *row_flags;
@@ -121,7 +122,8 @@ attn_split_kernel(const AttnArgs args) {
         if (!any) return;
     }
 
-    const int lo_j = chunk_lo(args.L, args.p, j), hi_j = chunk_hi(args.L, args.p, j);
+    const int Lb = args.seq_lens ? min(args.seq_lens[b], args.L) : args.L;
+    const int lo_j = chunk_lo(Lb, args.p, j), hi_j = chunk_hi(Lb, args.p, j);
     const int per = (hi_j - lo_j + args.nsub - 1) / args.nsub;
     const int k_begin = min(hi_j, lo_j + sub * per);
     const int k_end = min(hi_j, k_begin + per);
@@ -368,7 +370,7 @@ attn_split_kernel(const AttnArgs args) {
             // pass 3: chunk verdicts, row flag
             for (int jj = threadIdx.x; jj < args.p; jj += ATT_THREADS) {
                 int v = s_cviol[jj];
-                if (v == INT_MAX) v = s_unrep[jj] ? chunk_lo(args.L, args.p, jj) : -1;
+                if (v == INT_MAX) v = s_unrep[jj] ? chunk_lo(Lb, args.p, jj) : -1;
                 if (args.viol_index) args.viol_index[row * args.p + jj] = v;
                 if (args.chunk_den) args.chunk_den[row * args.p + jj] = s_cviol[jj] == INT_MAX ? s_cden[jj] : 0.f;
                 if (v >= 0) s_any_flag = 1;
@@ -565,6 +567,7 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     a.q_sb = p->q_stride_b; a.q_sh = p->q_stride_h;
     a.kv_sb = p->kv_stride_b; a.kv_sh = p->kv_stride_h;
     a.o_sb = p->o_stride_b; a.o_sh = p->o_stride_h;
+    a.seq_lens = p->seq_lens;
     a.scale = p->scale; a.phi = p->phi; a.a = p->a; a.b = p->b;
     a.p = lay.p; a.nsub = lay.nsub;
     a.row_flags = p->row_flags; a.viol_index = p->viol_index; a.rows_recomputed = p->rows_recomputed;

@@ -109,9 +109,13 @@ __global__ void argmax_kernel(const T *__restrict__ logits, int32_t *__restrict_
     }
 }
 
-__global__ void advance_kernel(int32_t *pos, int B) {
+__global__ void advance_kernel(int32_t *pos, int32_t *lens, int B) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < B) pos[b] += 1;
+    if (b < B) {
+        const int p = pos[b] + 1;
+        pos[b] = p;
+        if (lens) lens[b] = p + 1;
+    }
 }
 
 }  // namespace fdpp
@@ -182,9 +186,9 @@ extern "C" fdpp_status fdpp_argmax(const void *logits, int32_t *ids, int32_t row
     return FDPP_OK;
 }
 
-extern "C" fdpp_status fdpp_advance_positions(int32_t *pos, int32_t B, void *stream) {
+extern "C" fdpp_status fdpp_advance_positions(int32_t *pos, int32_t *lens, int32_t B, void *stream) {
     FDPP_REQUIRE(B >= 1, FDPP_ERR_SHAPE, "B");
-    advance_kernel<<<ceil_div(B, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(pos, B);
+    advance_kernel<<<ceil_div(B, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(pos, lens, B);
     FDPP_CHECK_LAUNCH("advance_kernel");
     return FDPP_OK;
 }

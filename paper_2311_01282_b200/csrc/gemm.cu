@@ -51,7 +51,7 @@ constexpr int GEMV_WARPS = 8;
 template <typename T, int MR>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
 gemv_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W, int64_t ldw,
-            T *__restrict__ C, int64_t ldc, const T *R, int64_t ldr, int M, int N, int K) {
+            T *C, int64_t ldc, const T *R, int64_t ldr, int M, int N, int K) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.x * GEMV_NR;
     const int nchunks = K >> 3;  // 8 elements per 16-B chunk (K % 8 == 0 by contract)
@@ -136,7 +136,7 @@ struct TcSmem {
 template <typename T, int BW, int BX, bool SWAP, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-               T *__restrict__ C, int64_t ldc, const T *R, int64_t ldr, int M, int N, int K,
+               T *C, int64_t ldc, const T *R, int64_t ldr, int M, int N, int K,
                int kb_per_split, int splits, float *__restrict__ ws, int *__restrict__ counters) {
     using S = TcSmem<BW, BX, STAGES>;
     constexpr int MMA_M = SWAP ? BW : BX;

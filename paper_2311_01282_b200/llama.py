@@ -1,0 +1,223 @@
+"""Llama-family decode step on the three hot paths (the
+reference's toy caller is pipeline.py:88-163).
+
+One decode step for a batch of B sequences, all in libfdpp kernels:
+
+    embed -> L x [ rmsnorm -> QKV GEMM -> RoPE + KV append -> async attention
+                   (+ flagged-row recompute) -> O GEMM (+residual fused) ->
+                   rmsnorm -> gate|up GEMM -> SiLU*up -> down GEMM (+residual) ]
+          -> rmsnorm -> LM-head GEMM -> argmax -> advance positions
+
+Every GEMM goes through the heuristic dispatch table (ImplA/B/C chosen per
+[N, K] at M = B).  The whole step is captured once into a CUDA graph: the
+attended lengths live in device memory (``seq_lens``) and advance on the
+device, so replaying the same graph decodes successive tokens with no host
+work between kernels.
+
+Geometry is real Llama-2 (gate projection, RMSNorm, RoPE, residuals, LM
+head), not the reference's 4-GEMM toy layer; weights are random-init
+(N(0, 1/K)), the KV cache is prefilled with N(0, 1) synthetic state.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib, workspace
+from . import dispatch as _dispatch_mod  # noqa: F401  (module, not the function)
+from .attention import AttentionConfig, decode_attention
+from .gemm import PackedWeight
+from .softmax import ScalingCalibration
+
+import importlib
+
+D = importlib.import_module("paper_2311_01282_b200.dispatch")
+
+# calibrate(default_rng(0).normal(0, 2, 1e6), 0.9999, 1.0)
+GOLDEN_CALIB = ScalingCalibration(phi=-7.775933742523193, a=-1.0, b=16.577659606933594,
+                                  coverage=0.999989)
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    name: str
+    hidden: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    ffn: int
+    n_layers: int
+    vocab: int
+    rope_theta: float = 10000.0
+    eps: float = 1e-5
+
+    def gemm_shapes(self):
+        """[N, K] of each dispatched GEMM in one step."""
+        qkv = (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+        return {"qkv": (qkv, self.hidden), "o": (self.hidden, self.n_heads * self.head_dim),
+                "gate_up": (2 * self.ffn, self.hidden), "down": (self.hidden, self.ffn),
+                "lm_head": (self.vocab, self.hidden)}
+
+    def weight_bytes(self, dtype_bytes=2) -> int:
+        per_layer = sum(n * k for n, k in list(self.gemm_shapes().values())[:4]) + 2 * self.hidden
+        return dtype_bytes * (self.n_layers * per_layer + 2 * self.vocab * self.hidden + self.hidden)
+
+    def kv_bytes_per_token(self, dtype_bytes=2) -> int:
+        return 2 * self.n_layers * self.n_kv_heads * self.head_dim * dtype_bytes
+
+
+LLAMA2_7B = LlamaConfig("llama2-7b", 4096, 32, 32, 128, 11008, 32, 32000)
+LLAMA2_70B = LlamaConfig("llama2-70b", 8192, 64, 8, 128, 28672, 80, 32000)
+CHATGLM2_6B = LlamaConfig("chatglm2-6b", 4096, 32, 2, 128, 13696, 28, 65024)
+
+
+def build_dispatch_table(cfg: LlamaConfig, m_sweep=D.B200_M_SWEEP, reps=5, dtype=torch.float16,
+                         fingerprint=None):
+    """Profile every GEMM shape of a decode step on this device (profile_shape)."""
+    table = D.DispatchTable(fingerprint=fingerprint or D.default_fingerprint())
+    for n, k in sorted(set(cfg.gemm_shapes().values())):
+        table.add(D.profile_shape(n, k, m_sweep=m_sweep, reps=reps, dtype=dtype))
+    return table
+
+
+class LlamaDecoder:
+    """Random-init Llama decode engine over libfdpp (one replica per GPU)."""
+
+    def __init__(self, cfg: LlamaConfig, batch: int, max_len: int, *, table=None,
+                 calib: ScalingCalibration = GOLDEN_CALIB, dtype=torch.float16, seed: int = 0,
+                 attn_p: int = 0, attn_splits: int = 0, n_layers: int = None):
+        _lib.require_cuda()
+        self.cfg, self.B, self.max_len, self.dtype = cfg, batch, max_len, dtype
+        self.n_layers = n_layers or cfg.n_layers
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        g = torch.Generator(device=dev).manual_seed(seed)
+        shapes = cfg.gemm_shapes()
+
+        def w(n, k):
+            t = torch.empty((n, k), dtype=dtype, device=dev)
+            t.normal_(0.0, 1.0 / math.sqrt(k), generator=g)
+            return PackedWeight(t, k, n)
+
+        self.layers = []
+        for _ in range(self.n_layers):
+            self.layers.append({
+                "qkv": w(*shapes["qkv"]), "o": w(*shapes["o"]),
+                "gate_up": w(*shapes["gate_up"]), "down": w(*shapes["down"]),
+                "ln1": torch.ones(cfg.hidden, dtype=dtype, device=dev),
+                "ln2": torch.ones(cfg.hidden, dtype=dtype, device=dev),
+            })
+        self.embed = torch.empty((cfg.vocab, cfg.hidden), dtype=dtype, device=dev).normal_(0, 1, generator=g)
+        self.lm_head = w(*shapes["lm_head"])
+        self.ln_f = torch.ones(cfg.hidden, dtype=dtype, device=dev)
+        Hq, Hkv, Dh = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+        self.k_cache = [torch.empty((batch, Hkv, max_len, Dh), dtype=dtype, device=dev)
+                        for _ in range(self.n_layers)]
+        self.v_cache = [torch.empty_like(self.k_cache[0]) for _ in range(self.n_layers)]
+        B = batch
+        self.x = torch.zeros((B, cfg.hidden), dtype=dtype, device=dev)
+        self.h = torch.zeros_like(self.x)
+        self.qkv = torch.zeros((B, shapes["qkv"][0]), dtype=dtype, device=dev)
+        self.q = torch.zeros((B, Hq, Dh), dtype=dtype, device=dev)
+        self.attn = torch.zeros((B, Hq, Dh), dtype=dtype, device=dev)
+        self.gu = torch.zeros((B, 2 * cfg.ffn), dtype=dtype, device=dev)
+        self.act = torch.zeros((B, cfg.ffn), dtype=dtype, device=dev)
+        self.logits = torch.zeros((B, cfg.vocab), dtype=dtype, device=dev)
+        self.ids = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.pos = torch.zeros(B, dtype=torch.int32, device=dev)
+        self.lens = torch.ones(B, dtype=torch.int32, device=dev)
+        self.row_flags = torch.zeros((B, Hq), dtype=torch.uint8, device=dev)
+        self.recomputed = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.attn_cfg = AttentionConfig(p=attn_p, scale=1.0 / math.sqrt(Dh), calib=calib,
+                                        splits_per_chunk=attn_splits)
+        if table is None:
+            table = build_dispatch_table(cfg, dtype=dtype)
+        self.table = table
+        self.choices = {op: D.dispatch(B, n, k, table) for op, (n, k) in shapes.items()}
+        self.graph = None
+        self.launches_per_step = 1 + self.n_layers * 10 + 4
+
+    # ------------------------------------------------------------------ state
+    def prefill_random(self, L: int, seed: int = 1):
+        """Synthetic prompt state: KV rows [0, L) ~ N(0, 1); next token at L."""
+        if L + 1 > self.max_len:
+            raise ValueError("prefill length exceeds the cache")
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        for kc, vc in zip(self.k_cache, self.v_cache):
+            kc[:, :, :L].normal_(0, 1, generator=g)
+            vc[:, :, :L].normal_(0, 1, generator=g)
+        self.pos.fill_(L)
+        self.lens.fill_(L + 1)
+        self.ids.random_(0, self.cfg.vocab, generator=g)
+
+    # ------------------------------------------------------------------ one step
+    def _gemm(self, op, a, pw, out, residual=None):
+        D.run_device(self.choices[op], a, pw, out=out, residual=residual, ws_tag="decode_gemm")
+
+    def enqueue_step(self):
+        """Enqueue one decode step on the current stream (no host sync)."""
+        cfg, B, dt = self.cfg, self.B, _lib.dtype_code(self.dtype)
+        lib = _lib.load()
+        st = _lib.stream_handle()
+        Hq, Hkv, Dh = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+        _lib.check(lib.fdpp_embed(self.ids.data_ptr(), self.embed.data_ptr(), self.x.data_ptr(), B,
+                                  cfg.hidden, dt, st), "embed")
+        for li, L in enumerate(self.layers):
+            _lib.check(lib.fdpp_rmsnorm(self.x.data_ptr(), L["ln1"].data_ptr(), self.h.data_ptr(), B,
+                                        cfg.hidden, cfg.eps, dt, st), "rmsnorm")
+            self._gemm("qkv", self.h, L["qkv"], self.qkv)
+            kc, vc = self.k_cache[li], self.v_cache[li]
+            _lib.check(lib.fdpp_rope_append(self.qkv.data_ptr(), self.q.data_ptr(), kc.data_ptr(),
+                                            vc.data_ptr(), self.pos.data_ptr(), B, Hq, Hkv, Dh,
+                                            kc.stride(0), kc.stride(1), cfg.rope_theta, dt, st),
+                       "rope_append")
+            decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
+                             seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed)
+            self._gemm("o", self.attn.view(B, Hq * Dh), L["o"], self.x, residual=self.x)
+            _lib.check(lib.fdpp_rmsnorm(self.x.data_ptr(), L["ln2"].data_ptr(), self.h.data_ptr(), B,
+                                        cfg.hidden, cfg.eps, dt, st), "rmsnorm")
+            self._gemm("gate_up", self.h, L["gate_up"], self.gu)
+            _lib.check(lib.fdpp_silu_mul(self.gu.data_ptr(), self.act.data_ptr(), B, cfg.ffn, dt, st),
+                       "silu_mul")
+            self._gemm("down", self.act, L["down"], self.x, residual=self.x)
+        _lib.check(lib.fdpp_rmsnorm(self.x.data_ptr(), self.ln_f.data_ptr(), self.h.data_ptr(), B,
+                                    cfg.hidden, cfg.eps, dt, st), "rmsnorm")
+        self._gemm("lm_head", self.h, self.lm_head, self.logits)
+        _lib.check(lib.fdpp_argmax(self.logits.data_ptr(), self.ids.data_ptr(), B, cfg.vocab, dt, st),
+                   "argmax")
+        _lib.check(lib.fdpp_advance_positions(self.pos.data_ptr(), self.lens.data_ptr(), B, st),
+                   "advance")
+
+    def capture(self):
+        """Capture one step into a CUDA graph (warms every kernel first)."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            saved = (self.pos.clone(), self.lens.clone(), self.ids.clone())
+            self.enqueue_step()                       # warm: attributes, tensor maps, workspaces
+            self.pos.copy_(saved[0]); self.lens.copy_(saved[1]); self.ids.copy_(saved[2])
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.enqueue_step()
+        torch.cuda.synchronize()
+        self.graph = g
+        return g
+
+    def step(self):
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+
+    def decode(self, ids_host, out_host):
+        """End-to-end step through the public API: H2D copy of this step's token
+        ids (pinned host int32 [B]), one graph replay, D2H of the next ids."""
+        self.ids.copy_(ids_host, non_blocking=True)
+        self.step()
+        out_host.copy_(self.ids, non_blocking=True)
+        return out_host

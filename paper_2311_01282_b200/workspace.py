@@ -22,7 +22,11 @@ def get(nbytes: int, device=None, tag: str = "default") -> torch.Tensor:
     (e.g. attention vs GEMM) or that a captured graph must own exclusively.
     """
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    key = (dev.index, tag, torch.cuda.current_stream(dev).cuda_stream)
+    # keyed by (device, tag), not by stream: a CUDA-graph capture must reuse the
+    # buffer its warm-up allocated (an allocation inside capture would add a
+    # zero-fill node to every replay).  Callers that run concurrently on
+    # several streams pass distinct tags.
+    key = (dev.index, tag)
     with _lock:
         buf = _pools.get(key)
         if buf is None or buf.numel() < max(nbytes, 1):
