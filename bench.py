@@ -254,7 +254,7 @@ def run_gpu(args):
     Lnow = int(dec.lens[0].item())
     attn_bytes = B * hkv * Lnow * dh * 2 * 2 + 2 * B * hq * dh * 2
     ops["attention_async(+recompute)"] = {"s_per_launch": t_attn, "bytes": attn_bytes,
-                                          "launches_per_step": 2 * dec.n_layers}
+                                          "launches_per_step": dec.n_layers}
     shapes = cfg.gemm_shapes()
     bufs = {"qkv": (dec.h, dec.qkv), "o": (dec.attn.view(B, hq * dh), dec.h),
             "gate_up": (dec.h, dec.gu), "down": (dec.act, dec.h), "lm_head": (dec.h, dec.logits)}

@@ -38,6 +38,11 @@ const char *fdpp_last_error(void);
 int fdpp_version(void);
 /* Streaming-multiprocessor count of the current device (148 on B200), or -1. */
 int fdpp_sm_count(void);
+/* Launch every kernel with programmatic dependent launch (default on): a
+ * kernel may start its prologue -- and a GEMM its weight stream -- while its
+ * predecessor in the stream finishes; each kernel waits (griddepcontrol.wait)
+ * before reading produced data or writing memory.  Returns the old setting. */
+int fdpp_set_pdl(int enable);
 
 /* ------------------------------------------------- subsystem 1: attention */
 typedef enum { FDPP_ATTN_ASYNC = 0, FDPP_ATTN_SYNC = 1 } fdpp_attn_mode;
@@ -108,11 +113,17 @@ typedef struct fdpp_gemm_params {
     int32_t M, N, K;
     int32_t dtype;                /* FDPP_F16 or FDPP_BF16                     */
     int32_t block_x;              /* ImplB/C token-tile rows; 0 = auto         */
-    int32_t splits;               /* split-K factor; 0 = auto                  */
+    int32_t ctas;                 /* 0 = auto: ImplB with fewer 128-row tiles
+                                     than SMs uses cluster split-K (DSMEM
+                                     reduction), otherwise a persistent
+                                     stream-K grid of one CTA per SM; > 0 =
+                                     stream-K with this many CTAs; < 0 =
+                                     cluster split-K with -ctas CTAs/cluster   */
     int32_t stages;               /* smem ring depth; 0 = auto (1 = single
                                      buffer, 2 = the paper's double buffer)     */
-    void *workspace;              /* split-K partials + tile counters (zeroed
-                                     before first use, left zeroed)            */
+    void *workspace;              /* stream-K partials of split tiles + tile
+                                     counters (zeroed before first use, left
+                                     zeroed)                                    */
     size_t workspace_bytes;
 } fdpp_gemm_params;
 
@@ -126,8 +137,9 @@ fdpp_status fdpp_gemm_workspace_size(int32_t impl, const fdpp_gemm_params *p, si
 fdpp_status fdpp_impl_a_gemv(const fdpp_gemm_params *p, void *stream);
 /* ImplB (dispatch.py:140-145 / flatgemm.py:215-242): swap-AB tcgen05 flat
  * GEMM — weight rows on the MMA M axis (128), tokens on the MMA N axis
- * (16..64, TMA zero-fills the padding), TMA/mbarrier ring, N-split grid with
- * deterministic split-K. */
+ * (16..64, TMA zero-fills the padding), persistent stream-K grid over the
+ * (N-tile, k-block) space with one continuous TMA/mbarrier ring per SM,
+ * double-buffered TMEM accumulators, fixed-order fixup of split tiles. */
 fdpp_status fdpp_impl_b_flat(const fdpp_gemm_params *p, void *stream);
 /* ImplC (dispatch.py:117-137): conventional tcgen05 GEMM, tokens on the MMA
  * M axis (128-row tiles). */

@@ -44,7 +44,7 @@ class GemmParams(ctypes.Structure):
         ("a", c_vp), ("lda", c_i64), ("w", c_vp), ("ldw", c_i64), ("c", c_vp), ("ldc", c_i64),
         ("r", c_vp), ("ldr", c_i64),
         ("M", c_i32), ("N", c_i32), ("K", c_i32), ("dtype", c_i32),
-        ("block_x", c_i32), ("splits", c_i32), ("stages", c_i32),
+        ("block_x", c_i32), ("ctas", c_i32), ("stages", c_i32),
         ("workspace", c_vp), ("workspace_bytes", c_sz),
     ]
 
@@ -54,6 +54,7 @@ SIGNATURES = {
     "fdpp_last_error": (ctypes.c_char_p, []),
     "fdpp_version": (ctypes.c_int, []),
     "fdpp_sm_count": (ctypes.c_int, []),
+    "fdpp_set_pdl": (ctypes.c_int, [ctypes.c_int]),
     "fdpp_attn_workspace_size": (c_i32, [ctypes.POINTER(AttnParams), ctypes.POINTER(c_sz)]),
     "fdpp_attn_plan": (c_i32, [ctypes.POINTER(AttnParams), ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "fdpp_attn_decode": (c_i32, [ctypes.POINTER(AttnParams), c_vp]),

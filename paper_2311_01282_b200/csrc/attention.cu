@@ -116,10 +116,14 @@ attn_split_kernel(const AttnArgs args) {
     const int gcount = min(GT, args.G - g0);
     const int h0 = kvh * args.G + g0;         // first query head of this row group
 
+    pdl_wait();  // q, the appended K/V row and row_flags come from earlier kernels
     if (!ASYNC && args.only_flagged) {        // recompute launch: skip clean row groups
         int any = 0;
         for (int g = 0; g < gcount; ++g) any |= args.row_flags[(int64_t)b * args.Hq + h0 + g];
-        if (!any) return;
+        if (!any) {
+            pdl_trigger();
+            return;
+        }
     }
 
     const int Lb = args.seq_lens ? min(args.seq_lens[b], args.L) : args.L;
@@ -268,6 +272,7 @@ attn_split_kernel(const AttnArgs args) {
                 }
             }
         }
+        pdl_trigger();  // main stream done: the next kernel may start its prologue
         // ---- per-warp partials to shared memory: red[w][g][0..D) = num, [D] = den, [D+1] = m/viol
         if (kg == 0) {
 #pragma unroll
@@ -330,19 +335,34 @@ attn_split_kernel(const AttnArgs args) {
     if (!s_last) return;
     __threadfence();
 
+    constexpr int LB = 32;  // partial loads kept in flight per thread
     for (int g = 0; g < gcount; ++g) {
         const int64_t row = row0 + g;
         const int64_t base = row * P;
         if (!ASYNC && args.only_flagged && !args.row_flags[row]) continue;
         T *op = static_cast<T *>(args.o) + (int64_t)b * args.o_sb + (int64_t)(h0 + g) * args.o_sh;
+        const int nsub = args.nsub;
         if (ASYNC) {
-            // pass 1: chunk exp-sums and first violation per chunk
+            // pass 1: chunk exp-sums and first violation per chunk (one thread per chunk,
+            // its nsub partials loaded LB at a time)
             for (int jj = threadIdx.x; jj < args.p; jj += ATT_THREADS) {
                 float cd = 0.f;
                 int vm = INT_MAX;
-                for (int s = 0; s < args.nsub; ++s) {
-                    cd += ld_cg_f32(&args.ws_den[base + jj * args.nsub + s]);
-                    vm = min(vm, __ldcg(&args.ws_viol[base + jj * args.nsub + s]));
+                for (int s0 = 0; s0 < nsub; s0 += LB) {
+                    float dv[LB];
+                    int vv[LB];
+#pragma unroll
+                    for (int q = 0; q < LB; ++q) {
+                        const bool ok = s0 + q < nsub;
+                        const int64_t i = base + (int64_t)jj * nsub + s0 + q;
+                        dv[q] = ok ? ld_cg_f32(&args.ws_den[i]) : 0.f;
+                        vv[q] = ok ? __ldcg(&args.ws_viol[i]) : INT_MAX;
+                    }
+#pragma unroll
+                    for (int q = 0; q < LB; ++q) {
+                        cd += dv[q];
+                        vm = min(vm, vv[q]);
+                    }
                 }
                 s_cden[jj] = cd;
                 s_cviol[jj] = vm;
@@ -350,19 +370,33 @@ attn_split_kernel(const AttnArgs args) {
             }
             if (threadIdx.x == 0) s_any_flag = 0;
             __syncthreads();
-            // pass 2: chunk numerators (non-finite chunk state => violation, attention.py:230-237)
+            // pass 2: chunk numerators over the flattened (chunk, sub) partials, LB loads
+            // in flight; a non-finite chunk state is a violation (attention.py:230-237)
             float tot[(D + ATT_THREADS - 1) / ATT_THREADS];
             int nd = 0;
             for (int d = threadIdx.x; d < D; d += ATT_THREADS, ++nd) {
-                float acc = 0.f;
-                for (int jj = 0; jj < args.p; ++jj) {
-                    float cn = 0.f;
-                    for (int s = 0; s < args.nsub; ++s)
-                        cn += ld_cg_f32(&args.ws_num[(base + jj * args.nsub + s) * D + d]);
-                    if (!isfinite(cn)) s_unrep[jj] = 1;  // benign race: all writers store 1
-                    if (args.chunk_num)  // chunk state; a violating chunk is zeroed (attention.py:191-194)
-                        args.chunk_num[(row * args.p + jj) * D + d] = s_cviol[jj] == INT_MAX ? cn : 0.f;
-                    acc += cn;
+                float acc = 0.f, cn = 0.f;
+                for (int i0 = 0; i0 < P; i0 += LB) {
+                    float val[LB];
+#pragma unroll
+                    for (int q = 0; q < LB; ++q)
+                        val[q] = i0 + q < P ? ld_cg_f32(&args.ws_num[(base + i0 + q) * D + d]) : 0.f;
+#pragma unroll
+                    for (int q = 0; q < LB; ++q) {
+                        const int i = i0 + q;
+                        if (i < P) {
+                            cn += val[q];
+                            if ((i + 1) % nsub == 0) {  // chunk jj complete, in sub order
+                                const int jj = i / nsub;
+                                if (!isfinite(cn)) s_unrep[jj] = 1;  // benign race: all store 1
+                                if (args.chunk_num)  // zeroed for a violating chunk (attention.py:191-194)
+                                    args.chunk_num[(row * args.p + jj) * D + d] =
+                                        s_cviol[jj] == INT_MAX ? cn : 0.f;
+                                acc += cn;
+                                cn = 0.f;
+                            }
+                        }
+                    }
                 }
                 tot[nd] = acc;
             }
@@ -390,19 +424,40 @@ attn_split_kernel(const AttnArgs args) {
             }
             __syncthreads();
         } else {
-            // Eq. (2) join over all (chunk, sub-range) partials in index order
+            // Eq. (2) join over all (chunk, sub-range) partials in index order;
+            // the per-partial maxima and scaled sums are staged in smem first
+            float *s_m = s_cden;                       // [P] maxima (P <= 2*ATT_MAX_P)
+            float *s_f = reinterpret_cast<float *>(s_cviol);
+            for (int i = threadIdx.x; i < P; i += ATT_THREADS) s_m[i] = ld_cg_f32(&args.ws_m[base + i]);
+            __syncthreads();
             float mrow = -INFINITY;
-            for (int i = 0; i < P; ++i) mrow = fmaxf(mrow, ld_cg_f32(&args.ws_m[base + i]));
+            for (int i = 0; i < P; ++i) mrow = fmaxf(mrow, s_m[i]);
+            __syncthreads();
+            for (int i = threadIdx.x; i < P; i += ATT_THREADS) s_f[i] = safe_scale(s_m[i], mrow);
+            __syncthreads();
             float l = 0.f;
-            for (int i = 0; i < P; ++i)
-                l += ld_cg_f32(&args.ws_den[base + i]) * safe_scale(ld_cg_f32(&args.ws_m[base + i]), mrow);
+            for (int i0 = 0; i0 < P; i0 += LB) {
+                float dv[LB];
+#pragma unroll
+                for (int q = 0; q < LB; ++q) dv[q] = i0 + q < P ? ld_cg_f32(&args.ws_den[base + i0 + q]) : 0.f;
+#pragma unroll
+                for (int q = 0; q < LB; ++q)
+                    if (i0 + q < P) l += dv[q] * s_f[i0 + q];
+            }
             for (int d = threadIdx.x; d < D; d += ATT_THREADS) {
                 float acc = 0.f;
-                for (int i = 0; i < P; ++i)
-                    acc += ld_cg_f32(&args.ws_num[(base + i) * D + d]) *
-                           safe_scale(ld_cg_f32(&args.ws_m[base + i]), mrow);
+                for (int i0 = 0; i0 < P; i0 += LB) {
+                    float val[LB];
+#pragma unroll
+                    for (int q = 0; q < LB; ++q)
+                        val[q] = i0 + q < P ? ld_cg_f32(&args.ws_num[(base + i0 + q) * D + d]) : 0.f;
+#pragma unroll
+                    for (int q = 0; q < LB; ++q)
+                        if (i0 + q < P) acc += val[q] * s_f[i0 + q];
+                }
                 op[d] = Elem<T>::from_f(acc / l);
             }
+            __syncthreads();
         }
     }
 }
@@ -431,9 +486,9 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
         FDPP_REQUIRE(p->p <= ATT_MAX_P, FDPP_ERR_VALUE, "partition count above %d", ATT_MAX_P);
         lay->p = p->p;
     } else {
-        // auto: enough chunks to give ~2 waves of CTAs, >= 128 keys per chunk
-        int want = (2 * sms + groups - 1) / groups;
-        int maxp = p->L / 128 > 0 ? p->L / 128 : 1;
+        // auto: enough chunks for ~8 CTAs per SM over the launch, >= 512 keys each
+        int want = (8 * sms + groups - 1) / groups;
+        int maxp = p->L / 512 > 0 ? p->L / 512 : 1;
         lay->p = want < 1 ? 1 : (want > maxp ? maxp : want);
         if (lay->p > ATT_MAX_P) lay->p = ATT_MAX_P;
     }
@@ -441,11 +496,13 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
         lay->nsub = p->splits_per_chunk;
     } else {
         const int per_chunk = p->L / lay->p;
-        int want = (2 * sms + groups * lay->p - 1) / (groups * lay->p);
-        int maxs = per_chunk / 64 > 0 ? per_chunk / 64 : 1;  // >= 64 keys per CTA
+        int want = (8 * sms + groups * lay->p - 1) / (groups * lay->p);
+        int maxs = per_chunk / 512 > 0 ? per_chunk / 512 : 1;  // >= 512 keys per CTA
         lay->nsub = want < 1 ? 1 : (want > maxs ? maxs : want);
     }
     lay->P = lay->p * lay->nsub;
+    FDPP_REQUIRE(lay->P <= ATT_MAX_P, FDPP_ERR_VALUE,
+                 "p x splits_per_chunk = %d exceeds %d partials per row", lay->P, ATT_MAX_P);
     const size_t rows = (size_t)p->B * p->Hq;
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     size_t off = 0;
@@ -472,8 +529,8 @@ static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st) {
         attr = true;
     }
     dim3 grid(grid_x, a.Hkv * a.n_rg, a.B);
-    kern<<<grid, ATT_THREADS, smem, st>>>(a);
-    FDPP_CHECK_LAUNCH("attn_split_kernel");
+    cudaError_t e = launch_kernel(kern, grid, dim3(ATT_THREADS), smem, st, a);
+    if (e != cudaSuccess) return cuda_status(e, "attn_split_kernel launch");
     return FDPP_OK;
 }
 

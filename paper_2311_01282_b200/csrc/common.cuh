@@ -9,6 +9,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/fdpp.h"
 
@@ -40,6 +41,45 @@ inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 // call can never see partial sums where it expects zeroed counters.
 constexpr int kWsCounters = 16384;
 constexpr size_t kWsCounterBytes = kWsCounters * sizeof(int);
+
+// Launch with the programmatic-stream-serialization attribute when PDL is
+// enabled (fdpp_set_pdl); every kernel in libfdpp calls pdl_wait() before
+// reading a predecessor's output or writing any global memory.
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block,
+                                         size_t smem, cudaStream_t st, int cluster_x,
+                                         Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (pdl_enabled()) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    if (cluster_x > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = cluster_x;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t st, Args &&...args) {
+    return launch_kernel_cluster(kern, grid, block, smem, st, 1, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------- element types
 template <typename T> struct Elem;
@@ -217,6 +257,61 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N, bool bf16) {
            | ((uint32_t)(N >> 3) << 17)      // N / 8
            | ((uint32_t)(M >> 4) << 24);     // M / 16
 }
+
+// Programmatic dependent launch (PDL).  Kernels launched with
+// launch_kernel() may start before their predecessor in the stream finishes:
+// everything before pdl_wait() must touch only data no earlier kernel writes
+// (weights, tensor maps, smem/TMEM setup).  pdl_wait() returns once every
+// prerequisite grid has completed and its writes are visible; it is a no-op
+// when the launch had no programmatic dependency.
+__device__ __forceinline__ void pdl_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+// Allow the next kernel in the stream to begin launching (its pdl_wait()
+// still waits for this whole grid to finish).
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ clusters
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// address of `local_smem` in the shared memory of cluster CTA `rank`
+__device__ __forceinline__ uint32_t dsmem_map(const void *local_smem, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local_smem)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float dsmem_ld_f32(uint32_t cluster_addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Trace build only (-DFDPP_TRACE): per-CTA event timestamps for the dev tools.
+#ifdef FDPP_TRACE
+// [launch % 8][cta][slot]; the launch number comes from a per-CTA-index counter
+static __device__ unsigned long long g_fdpp_trace[8][512][8];  // one TU (gemm.cu) uses it
+static __device__ unsigned int g_fdpp_launch[512];
+#define FDPP_TRACE_AT(slot)                                                       \
+    do {                                                                          \
+        if (blockIdx.x < 512) g_fdpp_trace[s_trace_seq & 7][blockIdx.x][slot] = globaltimer_ns(); \
+    } while (0)
+#else
+#define FDPP_TRACE_AT(slot) do { } while (0)
+#endif
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

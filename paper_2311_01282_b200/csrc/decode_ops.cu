@@ -9,6 +9,8 @@ namespace fdpp {
 template <typename T>
 __global__ void rmsnorm_kernel(const T *__restrict__ x, const T *__restrict__ w, T *__restrict__ out,
                                int dim, float eps) {
+    pdl_wait();
+    pdl_trigger();
     const int row = blockIdx.x;
     const T *xr = x + (int64_t)row * dim;
     float ss = 0.f;
@@ -36,6 +38,8 @@ template <typename T>
 __global__ void rope_append_kernel(const T *__restrict__ qkv, T *__restrict__ q_out, T *__restrict__ kc,
                                    T *__restrict__ vc, const int32_t *__restrict__ pos, int Hq, int Hkv,
                                    int D, int64_t csb, int64_t csh, float theta) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.x;
     const int half = D / 2;
     const int width = (Hq + 2 * Hkv) * D;
@@ -68,6 +72,8 @@ __global__ void rope_append_kernel(const T *__restrict__ qkv, T *__restrict__ q_
 
 template <typename T>
 __global__ void silu_mul_kernel(const T *__restrict__ gu, T *__restrict__ out, int F) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.y;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
         const float g = Elem<T>::to_f(gu[(int64_t)r * 2 * F + j]);
@@ -79,6 +85,8 @@ __global__ void silu_mul_kernel(const T *__restrict__ gu, T *__restrict__ out, i
 template <typename T>
 __global__ void embed_kernel(const int32_t *__restrict__ ids, const T *__restrict__ table,
                              T *__restrict__ out, int dim) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.x;
     const int64_t id = ids[b];
     for (int i = threadIdx.x; i < dim; i += blockDim.x) out[(int64_t)b * dim + i] = table[id * dim + i];
@@ -86,6 +94,8 @@ __global__ void embed_kernel(const int32_t *__restrict__ ids, const T *__restric
 
 template <typename T>
 __global__ void argmax_kernel(const T *__restrict__ logits, int32_t *__restrict__ ids, int vocab) {
+    pdl_wait();
+    pdl_trigger();
     const int r = blockIdx.x;
     float best = -INFINITY;
     int bi = 0x7fffffff;
@@ -110,6 +120,8 @@ __global__ void argmax_kernel(const T *__restrict__ logits, int32_t *__restrict_
 }
 
 __global__ void advance_kernel(int32_t *pos, int32_t *lens, int B) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b < B) {
         const int p = pos[b] + 1;
@@ -134,10 +146,11 @@ extern "C" fdpp_status fdpp_rmsnorm(const void *x, const void *w, void *out, int
                                     int32_t dim, float eps, int32_t dtype, void *stream) {
     FDPP_REQUIRE(rows >= 1 && dim >= 1, FDPP_ERR_SHAPE, "rmsnorm dims");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    FDPP_DT_SWITCH(dtype, rmsnorm_kernel<T><<<rows, 512, 0, st>>>(
-                              static_cast<const T *>(x), static_cast<const T *>(w),
-                              static_cast<T *>(out), dim, eps));
-    FDPP_CHECK_LAUNCH("rmsnorm_kernel");
+    cudaError_t e = cudaSuccess;
+    FDPP_DT_SWITCH(dtype, e = launch_kernel(rmsnorm_kernel<T>, dim3(rows), dim3(512), 0, st,
+                                            static_cast<const T *>(x), static_cast<const T *>(w),
+                                            static_cast<T *>(out), (int)dim, eps));
+    if (e != cudaSuccess) return cuda_status(e, "rmsnorm_kernel launch");
     return FDPP_OK;
 }
 
@@ -147,11 +160,12 @@ extern "C" fdpp_status fdpp_rope_append(const void *qkv, void *q_out, void *k_ca
                                         int32_t dtype, void *stream) {
     FDPP_REQUIRE(B >= 1 && Hq >= 1 && Hkv >= 1 && D >= 2 && D % 2 == 0, FDPP_ERR_SHAPE, "rope dims");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    FDPP_DT_SWITCH(dtype, rope_append_kernel<T><<<B, 512, 0, st>>>(
-                              static_cast<const T *>(qkv), static_cast<T *>(q_out),
-                              static_cast<T *>(k_cache), static_cast<T *>(v_cache), pos, Hq, Hkv,
-                              D, csb, csh, theta));
-    FDPP_CHECK_LAUNCH("rope_append_kernel");
+    cudaError_t e = cudaSuccess;
+    FDPP_DT_SWITCH(dtype, e = launch_kernel(rope_append_kernel<T>, dim3(B), dim3(512), 0, st,
+                                            static_cast<const T *>(qkv), static_cast<T *>(q_out),
+                                            static_cast<T *>(k_cache), static_cast<T *>(v_cache),
+                                            pos, (int)Hq, (int)Hkv, (int)D, csb, csh, theta));
+    if (e != cudaSuccess) return cuda_status(e, "rope_append_kernel launch");
     return FDPP_OK;
 }
 
@@ -160,9 +174,10 @@ extern "C" fdpp_status fdpp_silu_mul(const void *gu, void *out, int32_t rows, in
     FDPP_REQUIRE(rows >= 1 && F >= 1, FDPP_ERR_SHAPE, "silu_mul dims");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     dim3 grid(ceil_div(F, 256) < 16 ? ceil_div(F, 256) : 16, rows);
-    FDPP_DT_SWITCH(dtype, silu_mul_kernel<T><<<grid, 256, 0, st>>>(static_cast<const T *>(gu),
-                                                                   static_cast<T *>(out), F));
-    FDPP_CHECK_LAUNCH("silu_mul_kernel");
+    cudaError_t e = cudaSuccess;
+    FDPP_DT_SWITCH(dtype, e = launch_kernel(silu_mul_kernel<T>, grid, dim3(256), 0, st,
+                                            static_cast<const T *>(gu), static_cast<T *>(out), (int)F));
+    if (e != cudaSuccess) return cuda_status(e, "silu_mul_kernel launch");
     return FDPP_OK;
 }
 
@@ -170,9 +185,11 @@ extern "C" fdpp_status fdpp_embed(const int32_t *ids, const void *table, void *o
                                   int32_t dim, int32_t dtype, void *stream) {
     FDPP_REQUIRE(B >= 1 && dim >= 1, FDPP_ERR_SHAPE, "embed dims");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    FDPP_DT_SWITCH(dtype, embed_kernel<T><<<B, 256, 0, st>>>(ids, static_cast<const T *>(table),
-                                                             static_cast<T *>(out), dim));
-    FDPP_CHECK_LAUNCH("embed_kernel");
+    cudaError_t e = cudaSuccess;
+    FDPP_DT_SWITCH(dtype, e = launch_kernel(embed_kernel<T>, dim3(B), dim3(256), 0, st, ids,
+                                            static_cast<const T *>(table), static_cast<T *>(out),
+                                            (int)dim));
+    if (e != cudaSuccess) return cuda_status(e, "embed_kernel launch");
     return FDPP_OK;
 }
 
@@ -180,15 +197,17 @@ extern "C" fdpp_status fdpp_argmax(const void *logits, int32_t *ids, int32_t row
                                    int32_t dtype, void *stream) {
     FDPP_REQUIRE(rows >= 1 && vocab >= 1, FDPP_ERR_SHAPE, "argmax dims");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    FDPP_DT_SWITCH(dtype, argmax_kernel<T><<<rows, 1024, 0, st>>>(static_cast<const T *>(logits),
-                                                                  ids, vocab));
-    FDPP_CHECK_LAUNCH("argmax_kernel");
+    cudaError_t e = cudaSuccess;
+    FDPP_DT_SWITCH(dtype, e = launch_kernel(argmax_kernel<T>, dim3(rows), dim3(1024), 0, st,
+                                            static_cast<const T *>(logits), ids, (int)vocab));
+    if (e != cudaSuccess) return cuda_status(e, "argmax_kernel launch");
     return FDPP_OK;
 }
 
 extern "C" fdpp_status fdpp_advance_positions(int32_t *pos, int32_t *lens, int32_t B, void *stream) {
     FDPP_REQUIRE(B >= 1, FDPP_ERR_SHAPE, "B");
-    advance_kernel<<<ceil_div(B, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(pos, lens, B);
-    FDPP_CHECK_LAUNCH("advance_kernel");
+    cudaError_t e = launch_kernel(advance_kernel, dim3(ceil_div(B, 256)), dim3(256), 0,
+                                  static_cast<cudaStream_t>(stream), pos, lens, (int)B);
+    if (e != cudaSuccess) return cuda_status(e, "advance_kernel launch");
     return FDPP_OK;
 }

@@ -55,6 +55,7 @@ gemv_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W, int64
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.x * GEMV_NR;
     const int nchunks = K >> 3;  // 8 elements per 16-B chunk (K % 8 == 0 by contract)
+    pdl_wait();
     float acc[GEMV_NR][MR];
 #pragma unroll
     for (int r = 0; r < GEMV_NR; ++r)
@@ -88,6 +89,7 @@ gemv_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W, int64
             }
         }
     }
+    pdl_trigger();
     // warp reduction (fixed butterfly order)
 #pragma unroll
     for (int r = 0; r < GEMV_NR; ++r)
@@ -119,8 +121,22 @@ gemv_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W, int64
 }
 
 // ============================================================ ImplB / ImplC: tcgen05
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner + MMA
-// issuer, warps 2..5 = epilogue (TMEM lane quadrant = warp % 4).
+// Persistent stream-K kernel.  The (tile, k-block) iteration space -- tiles
+// ordered m-tile-major so consecutive tiles share the activation tile -- is
+// cut into one contiguous range of `units` k-blocks per CTA (one CTA per SM).
+// Inside a CTA:
+//   warp 0      TMA producer: streams W and X k-blocks of the whole range
+//               through one STAGES-deep smem ring, crossing tile boundaries
+//               without draining (the paper's double buffer, generalised);
+//   warp 1      TMEM owner + single-thread MMA issuer: one accumulation
+//               "segment" per (tile, contiguous k-range), alternating between
+//               two TMEM accumulators so the epilogue of segment s overlaps
+//               the MMAs of segment s + 1;
+//   warps 2..5  epilogue (TMEM lane quadrant = warp % 4): a segment covering
+//               the whole K of its tile is written straight to C (+ residual);
+//               a tile split across CTAs deposits fp32 partials and the last
+//               arriving CTA (atomic ticket) sums them in fixed segment order,
+//               so results are bitwise reproducible for a given grid.
 constexpr int TC_BK = 64;  // 64 fp16 = 128 B rows: one SWIZZLE_128B atom wide
 constexpr int TC_THREADS = 192;
 
@@ -130,36 +146,299 @@ struct TcSmem {
     static constexpr uint32_t X_BYTES = BX * TC_BK * 2;
     static constexpr uint32_t STAGE_BYTES = W_BYTES + X_BYTES;
     static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
-    static constexpr uint32_t TOTAL = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 1024;  // + align slack
+    static constexpr uint32_t TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
 };
+
+struct TcWork {
+    int n_tiles_n, n_tiles_m, kb_total, units, max_seg;
+};
+
+// Store 16 accumulator columns of one TMEM lane (+ residual).  SWAP: lane =
+// weight row n, column = token m; otherwise lane = token m, column = n.
+template <typename T, int BW, bool SWAP>
+__device__ __forceinline__ void epi_store16(const float (&v)[16], T *C, int64_t ldc, const T *R,
+                                            int64_t ldr, int M, int N, int n0, int m0, int row,
+                                            int c0) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int n = SWAP ? n0 + row : n0 + c0 + j;
+        const int m = SWAP ? m0 + c0 + j : m0 + row;
+        if (n < N && m < M) {
+            float o = v[j];
+            if (R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
+            C[(int64_t)m * ldc + n] = Elem<T>::from_f(o);
+        }
+    }
+}
 
 template <typename T, int BW, int BX, bool SWAP, int STAGES>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-               T *C, int64_t ldc, const T *R, int64_t ldr, int M, int N, int K,
-               int kb_per_split, int splits, float *__restrict__ ws, int *__restrict__ counters) {
+               T *C, int64_t ldc, const T *R /* may alias C */, int64_t ldr, int M, int N,
+               const TcWork wk, float *__restrict__ ws, int *__restrict__ counters) {
     using S = TcSmem<BW, BX, STAGES>;
     constexpr int MMA_M = SWAP ? BW : BX;
     constexpr int MMA_N = SWAP ? BX : BW;
     static_assert(MMA_M == 128, "tcgen05 tile uses the 128-lane MMA");
     static_assert(MMA_N % 16 == 0 && MMA_N >= 16 && MMA_N <= 256, "MMA N");
-    constexpr uint32_t TMEM_COLS = MMA_N <= 32 ? 32 : MMA_N <= 64 ? 64 : MMA_N <= 128 ? 128 : 256;
+    constexpr uint32_t ACC_COLS = MMA_N;  // one accumulator
+    constexpr uint32_t TMEM_COLS = 2 * ACC_COLS <= 32 ? 32 : 2 * ACC_COLS <= 64 ? 64
+                                 : 2 * ACC_COLS <= 128 ? 128 : 2 * ACC_COLS <= 256 ? 256 : 512;
     constexpr uint32_t IDESC = umma_idesc_f16(MMA_M, MMA_N, std::is_same<T, __nv_bfloat16>::value);
+    constexpr int TILE_ELEMS = BW * BX;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                 ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);
     uint64_t *empty = full + STAGES;
-    uint64_t *tmem_full = empty + STAGES;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+    uint64_t *tmem_full = empty + STAGES;      // [2]
+    uint64_t *tmem_empty = tmem_full + 2;      // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
     __shared__ int s_is_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BW, split = blockIdx.y, m0 = blockIdx.z * BX;
-    const int kb_total = (K + TC_BK - 1) / TC_BK;
-    const int kb0 = split * kb_per_split;
-    const int nkb = min(kb_total, kb0 + kb_per_split) - kb0;
+    const int KB = wk.kb_total;
+    const int total = wk.n_tiles_n * wk.n_tiles_m * KB;
+    const int u0 = blockIdx.x * wk.units;
+    const int u1 = min(total, u0 + wk.units);
+    if (u0 >= u1) return;  // uniform per CTA (host sizes the grid so this never triggers)
+#ifdef FDPP_TRACE
+    __shared__ unsigned int s_trace_seq;
+    if (threadIdx.x == 0) {
+        const unsigned long long t_entry = globaltimer_ns();
+        s_trace_seq = blockIdx.x < 512 ? atomicAdd(&g_fdpp_launch[blockIdx.x], 1u) : 0u;
+        if (blockIdx.x < 512) g_fdpp_trace[s_trace_seq & 7][blockIdx.x][7] = t_entry;
+    }
+    __syncthreads();
+#endif
+    if (threadIdx.x == 0) FDPP_TRACE_AT(0);
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmW);
+        prefetch_tmap(&tmX);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tmem_full[b], 1);
+            mbar_init(&tmem_empty[b], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer over the whole unit range
+            // PDL: the weight stream does not depend on any earlier kernel, so
+            // the first ring's worth of W tiles is requested before waiting on
+            // the predecessor; activation tiles follow once its output is visible.
+            const int pre = min(u1 - u0, STAGES);
+            for (int i = 0; i < pre; ++i) {
+                const int u = u0 + i, t = u / KB, kb = u % KB;
+                mbar_arrive_expect_tx(&full[i], S::STAGE_BYTES);
+                tma_load_2d(smem + i * S::STAGE_BYTES, &tmW, &full[i], kb * TC_BK,
+                            (t % wk.n_tiles_n) * BW, kEvictFirst);
+            }
+            FDPP_TRACE_AT(1);
+            pdl_wait();
+            FDPP_TRACE_AT(2);
+            for (int i = 0; i < pre; ++i) {
+                const int u = u0 + i, t = u / KB, kb = u % KB;
+                tma_load_2d(smem + i * S::STAGE_BYTES + S::W_BYTES, &tmX, &full[i], kb * TC_BK,
+                            (t / wk.n_tiles_n) * BX, kEvictLast);
+            }
+            for (int u = u0 + pre, i = pre; u < u1; ++u, ++i) {
+                const int s = i % STAGES;
+                const uint32_t ph = (i / STAGES) & 1;
+                const int t = u / KB, kb = u % KB;
+                mbar_wait(&empty[s], ph ^ 1);
+                uint8_t *sw = smem + s * S::STAGE_BYTES;
+                mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+                tma_load_2d(sw, &tmW, &full[s], kb * TC_BK, (t % wk.n_tiles_n) * BW, kEvictFirst);
+                tma_load_2d(sw + S::W_BYTES, &tmX, &full[s], kb * TC_BK, (t / wk.n_tiles_n) * BX,
+                            kEvictLast);
+            }
+            pdl_trigger();  // every load issued: let the next kernel start its prologue
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            int seg = 0;
+            for (int u = u0, i = 0; u < u1; ++u, ++i) {
+                const int s = i % STAGES;
+                const uint32_t ph = (i / STAGES) & 1;
+                const int kb = u % KB;
+                const bool first = (u == u0) || kb == 0;
+                const bool last = (u == u1 - 1) || kb == KB - 1;
+                const int buf = seg & 1;
+                if (first) {
+                    mbar_wait(&tmem_empty[buf], ((seg >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                }
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                if (i == 0) FDPP_TRACE_AT(3);
+                if (u == u1 - 1) FDPP_TRACE_AT(4);
+                uint8_t *sw = smem + s * S::STAGE_BYTES;
+                uint8_t *sx = sw + S::W_BYTES;
+                const uint64_t da = umma_desc_sw128(SWAP ? sw : sx);
+                const uint64_t db = umma_desc_sw128(SWAP ? sx : sw);
+                const uint32_t dt = tmem_base + buf * ACC_COLS;
+#pragma unroll
+                for (int k = 0; k < TC_BK / 16; ++k)  // UMMA_K = 16: +32 B inside the swizzle atom
+                    umma_f16(dt, da + 2 * k, db + 2 * k, IDESC, (first && k == 0) ? 0u : 1u);
+                umma_commit(&empty[s]);  // frees the smem slot when these MMAs finish
+                if (last) {
+                    umma_commit(&tmem_full[buf]);
+                    ++seg;
+                }
+            }
+        }
+    } else {  // ---------------- epilogue warps 2..5
+        pdl_wait();  // residual / C / workspace belong to the stream's earlier kernels
+        const int quad = warp & 3;
+        const int row = quad * 32 + lane;  // TMEM lane = accumulator row
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        int seg = 0;
+        for (int u = u0; u < u1; ++seg) {
+            const int t = u / KB, kb_start = u % KB;
+            const int kb_end = min(KB, kb_start + (u1 - u));
+            u += kb_end - kb_start;
+            const int n0 = (t % wk.n_tiles_n) * BW, m0 = (t / wk.n_tiles_n) * BX;
+            const int buf = seg & 1;
+            const bool whole = kb_start == 0 && kb_end == KB;
+            int c_lo = 0, nseg = 1, segi = 0;
+            float *slot = nullptr;
+            if (!whole) {
+                c_lo = (t * KB) / wk.units;
+                nseg = ((t + 1) * KB - 1) / wk.units - c_lo + 1;
+                segi = blockIdx.x - c_lo;
+                slot = ws + ((int64_t)t * wk.max_seg + segi) * TILE_ELEMS;
+            }
+            mbar_wait(&tmem_full[buf], (seg >> 1) & 1);
+            tc_fence_after();
+            if (warp == 2 && lane == 0) FDPP_TRACE_AT(5);
+            // 16 accumulator columns at a time: compact code, few live registers
+#pragma unroll 1
+            for (int c0 = 0; c0 < MMA_N; c0 += 16) {
+                float v[16];
+                tmem_ld16(tmem_base + buf * ACC_COLS + lane_off + c0, v);
+                if (whole) {
+                    epi_store16<T, BW, SWAP>(v, C, ldc, R, ldr, M, N, n0, m0, row, c0);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)   // partial tile layout [BX m][BW n]
+                        slot[SWAP ? (c0 + j) * BW + row : row * BW + c0 + j] = v[j];
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[buf]);  // accumulator may be reused
+            if (whole) continue;
+            // ---- split tile: last arriving CTA reduces all segments in fixed order
+            __threadfence();
+            named_bar_sync(1, 128);
+            if (warp == 2 && lane == 0) {
+                const int ticket = atomicAdd(&counters[t], 1);
+                s_is_last = (ticket == nseg - 1);
+                if (s_is_last) counters[t] = 0;  // leave the workspace zeroed
+            }
+            named_bar_sync(1, 128);
+            const bool is_last = s_is_last;
+            named_bar_sync(1, 128);  // s_is_last is rewritten by the next split tile
+            if (!is_last) continue;
+            __threadfence();
+            const float *base = ws + (int64_t)t * wk.max_seg * TILE_ELEMS;
+#pragma unroll 1
+            for (int c0 = 0; c0 < MMA_N; c0 += 16) {
+                float acc[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+                // segments in groups of 4: all loads of a group are in flight
+                // together (one L2 round trip), then added in segment order
+#pragma unroll 1
+                for (int sg0 = 0; sg0 < nseg; sg0 += 4) {
+                    float val[4][16];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float *src = base + (int64_t)(sg0 + q) * TILE_ELEMS;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            val[q][j] = (sg0 + q < nseg)
+                                ? ld_cg_f32(src + (SWAP ? (c0 + j) * BW + row : row * BW + c0 + j))
+                                : 0.f;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) acc[j] += val[q][j];
+                }
+                epi_store16<T, BW, SWAP>(acc, C, ldc, R, ldr, M, N, n0, m0, row, c0);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) FDPP_TRACE_AT(6);
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, TMEM_COLS);
+    }
+}
+
+// ============================================================ ImplB: cluster split-K
+// For few output tiles (small N, e.g. [4096, K]): the K range of each 128-row
+// weight tile is split across the CS CTAs of one thread-block cluster.  Each
+// CTA streams its K slice through the TMA ring into its own TMEM accumulator;
+// after a cluster barrier the fp32 slices are reduced over DSMEM -- CTA r sums
+// column slice r across ranks 0..CS-1 in fixed order and writes C (+residual)
+// -- so there are no global partials, fences or tickets, and the result is
+// bitwise reproducible.  All CS * n_tiles CTAs are co-resident (one wave).
+struct TcCluster {
+    int n_tiles_n, kb_total, kb_per, cs;
+};
+
+template <int BX, int STAGES>
+struct ClSmem {
+    using S = TcSmem<128, BX, STAGES>;
+    static constexpr uint32_t RING = STAGES * S::STAGE_BYTES;
+    static constexpr uint32_t PART = BX * 128 * 4;  // fp32 partial [MMA_N][128]
+    static constexpr uint32_t BAR_OFF = RING > PART ? RING : PART;
+    static constexpr uint32_t TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+};
+
+template <typename T, int BX, int STAGES>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                    T *C, int64_t ldc, const T *R /* may alias C */, int64_t ldr, int M, int N,
+                    const TcCluster ck) {
+    constexpr int BW = 128;
+    using S = TcSmem<BW, BX, STAGES>;
+    constexpr int MMA_N = BX;
+    constexpr uint32_t TMEM_COLS = MMA_N <= 32 ? 32 : MMA_N <= 64 ? 64 : 128;
+    constexpr uint32_t IDESC = umma_idesc_f16(128, MMA_N, std::is_same<T, __nv_bfloat16>::value);
+    using CS = ClSmem<BX, STAGES>;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + CS::BAR_OFF);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tmem_full = empty + STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 2);
+    float *part = reinterpret_cast<float *>(smem);  // [MMA_N][128] after the ring drains
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int tn = blockIdx.x / ck.cs, tm = blockIdx.y;
+    const int n0 = tn * BW, m0 = tm * BX;
+    const int kb0 = (int)rank * ck.kb_per;
+    const int nkb = min(ck.kb_total, kb0 + ck.kb_per) - kb0;  // >= 1 (host guarantees)
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmW);
@@ -178,93 +457,85 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
-            for (int i = 0; i < nkb; ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                uint8_t *sw = smem + s * S::STAGE_BYTES;
-                uint8_t *sx = sw + S::W_BYTES;
-                mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-                const int kc = (kb0 + i) * TC_BK;
-                tma_load_2d(sw, &tmW, &full[s], kc, n0, kEvictFirst);  // weights: streamed once
-                tma_load_2d(sx, &tmX, &full[s], kc, m0, kEvictLast);   // activations: reused
+        if (lane == 0) {  // ---------------- TMA producer (weights first, PDL)
+            const int pre = min(nkb, STAGES);
+            for (int i = 0; i < pre; ++i) {
+                mbar_arrive_expect_tx(&full[i], S::STAGE_BYTES);
+                tma_load_2d(smem + i * S::STAGE_BYTES, &tmW, &full[i], (kb0 + i) * TC_BK, n0, kEvictFirst);
             }
+            pdl_wait();
+            for (int i = 0; i < pre; ++i)
+                tma_load_2d(smem + i * S::STAGE_BYTES + S::W_BYTES, &tmX, &full[i], (kb0 + i) * TC_BK,
+                            m0, kEvictLast);
+            for (int i = pre; i < nkb; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+                uint8_t *sw = smem + s * S::STAGE_BYTES;
+                mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+                tma_load_2d(sw, &tmW, &full[s], (kb0 + i) * TC_BK, n0, kEvictFirst);
+                tma_load_2d(sw + S::W_BYTES, &tmX, &full[s], (kb0 + i) * TC_BK, m0, kEvictLast);
+            }
+            pdl_trigger();
         }
+        __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer (single thread)
+        if (lane == 0) {  // ---------------- MMA issuer
             for (int i = 0; i < nkb; ++i) {
                 const int s = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                mbar_wait(&full[s], ph);
+                mbar_wait(&full[s], (i / STAGES) & 1);
                 tc_fence_after();
                 uint8_t *sw = smem + s * S::STAGE_BYTES;
-                uint8_t *sx = sw + S::W_BYTES;
-                const uint64_t da = umma_desc_sw128(SWAP ? sw : sx);
-                const uint64_t db = umma_desc_sw128(SWAP ? sx : sw);
+                const uint64_t da = umma_desc_sw128(sw);
+                const uint64_t db = umma_desc_sw128(sw + S::W_BYTES);
 #pragma unroll
-                for (int k = 0; k < TC_BK / 16; ++k)  // UMMA_K = 16: +32 B inside the swizzle atom
-                    umma_f16(tmem_base, da + 2 * k, db + 2 * k, IDESC, (i | k) != 0);
-                umma_commit(&empty[s]);  // frees the smem slot when these MMAs finish
+                for (int k = 0; k < TC_BK / 16; ++k)
+                    umma_f16(tmem_base, da + 2 * k, db + 2 * k, IDESC, (i == 0 && k == 0) ? 0u : 1u);
+                umma_commit(&empty[s]);
             }
             umma_commit(tmem_full);
         }
-    } else {  // ---------------- epilogue warps 2..5
+        __syncwarp();
+    } else {  // ---------------- epilogue warps: TMEM -> own smem partial [col][row]
         const int quad = warp & 3;
-        const int row = quad * 32 + lane;  // TMEM lane = accumulator row
+        const int row = quad * 32 + lane;
         mbar_wait(tmem_full, 0);
         tc_fence_after();
-        const bool split_k = splits > 1;
-        const int m_alloc = gridDim.z * BX;
 #pragma unroll 1
         for (int c0 = 0; c0 < MMA_N; c0 += 16) {
             float v[16];
             tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + c0, v);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                // SWAP: row = weight row (n), column = token (m).  !SWAP: transposed.
-                const int n = SWAP ? n0 + row : n0 + c0 + j;
-                const int m = SWAP ? m0 + c0 + j : m0 + row;
-                if (n < N && m < M) {
-                    if (split_k) {
-                        ws[((int64_t)split * m_alloc + m) * N + n] = v[j];
-                    } else {
-                        float o = v[j];
-                        if (R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
-                        C[(int64_t)m * ldc + n] = Elem<T>::from_f(o);
-                    }
-                }
-            }
-        }
-        if (split_k) {
-            // last CTA of this output tile reduces all splits in fixed order
-            __threadfence();
-            named_bar_sync(1, 128);
-            if (warp == 2 && lane == 0) {
-                const int tile = blockIdx.z * gridDim.x + blockIdx.x;
-                const int ticket = atomicAdd(&counters[tile], 1);
-                s_is_last = (ticket == splits - 1);
-                if (s_is_last) counters[tile] = 0;  // leave the workspace zeroed
-            }
-            named_bar_sync(1, 128);
-            if (s_is_last) {
-                __threadfence();
-                for (int c0 = 0; c0 < MMA_N; ++c0) {
-                    const int n = SWAP ? n0 + row : n0 + c0;
-                    const int m = SWAP ? m0 + c0 : m0 + row;
-                    if (n < N && m < M) {
-                        float o = 0.f;
-                        for (int sp = 0; sp < splits; ++sp)
-                            o += ld_cg_f32(&ws[((int64_t)sp * m_alloc + m) * N + n]);
-                        if (R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
-                        C[(int64_t)m * ldc + n] = Elem<T>::from_f(o);
-                    }
-                }
-            }
+            for (int j = 0; j < 16; ++j) part[(c0 + j) * 128 + row] = v[j];
         }
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();  // every rank's partial is in its smem
+    if (warp >= 2) {
+        pdl_wait();  // residual / C belong to earlier kernels
+        const int quad = warp & 3;
+        const int row = quad * 32 + lane;
+        const int n = n0 + row;
+        const int per = (MMA_N + ck.cs - 1) / ck.cs;
+        const int c_beg = (int)rank * per, c_end = min(MMA_N, c_beg + per);
+        uint32_t peer[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) peer[q] = q < ck.cs ? dsmem_map(part, q) : 0u;
+        for (int c = c_beg; c < c_end; ++c) {
+            const int m = m0 + c;
+            float vals[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                vals[q] = q < ck.cs ? dsmem_ld_f32(peer[q] + (uint32_t)((c * 128 + row) * 4)) : 0.f;
+            float o = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o += vals[q];  // rank order
+            if (n < N && m < M) {
+                if (R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
+                C[(int64_t)m * ldc + n] = Elem<T>::from_f(o);
+            }
+        }
+    }
+    cluster_sync_all();  // peers may still be reading this CTA's partial
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, TMEM_COLS);
@@ -350,7 +621,10 @@ static fdpp_status make_kmajor_map(CUtensorMap *out, const void *ptr, int64_t ro
 
 // ============================================================ host: planning
 struct TcPlan {
-    int bw, bx, splits, kb_per_split, stages, grid_n, grid_m;
+    int bw, bx, stages, grid;
+    TcWork wk;
+    bool cluster;    // ImplB cluster split-K (few tiles) instead of stream-K
+    TcCluster ck;
 };
 
 static int pick_block_x(int M, bool swap) {
@@ -360,78 +634,118 @@ static int pick_block_x(int M, bool swap) {
     return 64;
 }
 
-// Choose the split-K factor so that n_tiles x splits CTAs balance the 148 SMs:
-// minimise waves x (k-blocks per split), tie-break on fewer splits (less
-// partial traffic).  The paper's "parallelism-bounded small N" insight
-// on a 148-SM part.
-static int pick_splits(int tiles, int kb_total, int sms) {
-    int best = 1;
-    double best_cost = 1e30;
-    for (int s = 1; s <= 16 && s <= kb_total; ++s) {
-        const int per = (kb_total + s - 1) / s;
-        const int ctas = tiles * s;
-        const int waves = (ctas + sms - 1) / sms;
-        const double cost = (double)waves * per * (1.0 + 0.01 * s);
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = s;
-        }
-    }
-    return best;
-}
-
 static fdpp_status plan_tc(const fdpp_gemm_params *p, bool swap, TcPlan *pl) {
     const int kb_total = ceil_div(p->K, TC_BK);
     pl->bx = p->block_x > 0 ? p->block_x : pick_block_x(p->M, swap);
     if (swap) {
         FDPP_REQUIRE(pl->bx == 16 || pl->bx == 32 || pl->bx == 64, FDPP_ERR_VALUE,
                      "ImplB block_x must be 16, 32 or 64");
-        pl->bw = 128;
     } else {
         FDPP_REQUIRE(pl->bx == 128, FDPP_ERR_VALUE, "ImplC block_x must be 128");
-        pl->bw = 128;
     }
-    pl->grid_n = ceil_div(p->N, pl->bw);
-    pl->grid_m = ceil_div(p->M, pl->bx);
-    int splits = p->splits > 0 ? p->splits : pick_splits(pl->grid_n * pl->grid_m, kb_total, sm_count());
-    splits = splits > kb_total ? kb_total : splits;
-    pl->kb_per_split = ceil_div(kb_total, splits);
-    pl->splits = ceil_div(kb_total, pl->kb_per_split);  // no empty splits
+    pl->bw = 128;
+    TcWork &w = pl->wk;
+    w.n_tiles_n = ceil_div(p->N, pl->bw);
+    w.n_tiles_m = ceil_div(p->M, pl->bx);
+    w.kb_total = kb_total;
+    const int64_t total = (int64_t)w.n_tiles_n * w.n_tiles_m * kb_total;
+    FDPP_REQUIRE(total < (1ll << 31), FDPP_ERR_SHAPE, "GEMM too large");
+    const int sms = sm_count() > 0 ? sm_count() : 148;
+    const int tiles = w.n_tiles_n * w.n_tiles_m;
+    // Auto policy for ImplB (measured in-graph on B200 across the Llama shapes,
+    // tools/mode_sweep.py): few tiles -> cluster split-K, 8 CTAs per tile for
+    // <= 40 tiles (e.g. N = 4096), 2 per tile up to ~0.9 SMs of tiles (N = 12288);
+    // many tiles -> stream-K with two CTAs per SM.  ctas < 0 forces cs = -ctas.
+    pl->cluster = swap && ((p->ctas == 0 && tiles <= (sms * 9) / 10) || p->ctas < 0);
+    if (pl->cluster) {
+        int cs = p->ctas < 0 ? -p->ctas : (tiles <= 40 ? 8 : 2);
+        cs = cs < 1 ? 1 : (cs > 8 ? 8 : cs);
+        if (cs > kb_total) cs = kb_total;
+        TcCluster &c = pl->ck;
+        c.n_tiles_n = w.n_tiles_n;
+        c.kb_total = kb_total;
+        c.kb_per = (kb_total + cs - 1) / cs;
+        c.cs = (kb_total + c.kb_per - 1) / c.kb_per;  // no empty rank
+        pl->grid = w.n_tiles_n * c.cs;
+        pl->stages = p->stages > 0 ? p->stages : 0;
+        return FDPP_OK;
+    }
+    // persistent stream-K grid: one CTA per SM (or the `ctas` override),
+    // contiguous equal unit ranges -- perfect balance up to one k-block
+    int ctas = p->ctas > 0 ? p->ctas : (swap ? 2 * sms : sms);
+    if (ctas > total) ctas = (int)total;
+    w.units = (int)((total + ctas - 1) / ctas);
+    pl->grid = (int)((total + w.units - 1) / w.units);
+    w.max_seg = (kb_total + w.units - 1) / w.units + 1;
+    FDPP_REQUIRE(w.n_tiles_n * w.n_tiles_m <= kWsCounters, FDPP_ERR_SHAPE,
+                 "too many output tiles (%d)", w.n_tiles_n * w.n_tiles_m);
     pl->stages = p->stages > 0 ? p->stages : 0;
-    FDPP_REQUIRE(pl->splits == 1 || pl->grid_n * pl->grid_m <= kWsCounters, FDPP_ERR_SHAPE,
-                 "too many output tiles for split-K (%d)", pl->grid_n * pl->grid_m);
     return FDPP_OK;
 }
 
+static bool has_split_tiles(const TcPlan &pl) {
+    return !pl.cluster && (pl.wk.units % pl.wk.kb_total != 0 || pl.wk.units < pl.wk.kb_total);
+}
+
 static size_t tc_workspace(const TcPlan &pl, const fdpp_gemm_params *p) {
-    if (pl.splits <= 1) return 0;
-    const size_t part = (size_t)pl.splits * pl.grid_m * pl.bx * p->N * sizeof(float);
+    (void)p;
+    if (!has_split_tiles(pl)) return 0;
+    const size_t part = (size_t)pl.wk.n_tiles_n * pl.wk.n_tiles_m * pl.wk.max_seg * pl.bw * pl.bx *
+                        sizeof(float);
     return kWsCounterBytes + part;
+}
+
+template <typename T, int BX, int STAGES>
+static fdpp_status launch_cluster(const fdpp_gemm_params *p, const TcPlan &pl, const CUtensorMap &mw,
+                                  const CUtensorMap &mx, cudaStream_t st) {
+    using S = ClSmem<BX, STAGES>;
+    auto kern = gemm_cluster_kernel<T, BX, STAGES>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)S::TOTAL);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_cluster)");
+        attr_set = true;
+    }
+    cudaError_t e = launch_kernel_cluster(kern, dim3(pl.grid, pl.wk.n_tiles_m), dim3(TC_THREADS),
+                                          S::TOTAL, st, pl.ck.cs, mw, mx, static_cast<T *>(p->c),
+                                          p->ldc, static_cast<const T *>(p->r), p->ldr, p->M, p->N,
+                                          pl.ck);
+    if (e != cudaSuccess) return cuda_status(e, "gemm_cluster_kernel launch");
+    return FDPP_OK;
 }
 
 template <typename T, int BW, int BX, bool SWAP, int STAGES>
 static fdpp_status launch_tc(const fdpp_gemm_params *p, const TcPlan &pl, const CUtensorMap &mw,
                              const CUtensorMap &mx, cudaStream_t st) {
+    if constexpr (SWAP && BW == 128) {
+        if (pl.cluster) return launch_cluster<T, BX, STAGES>(p, pl, mw, mx, st);
+    }
     using S = TcSmem<BW, BX, STAGES>;
     auto kern = gemm_tc_kernel<T, BW, BX, SWAP, STAGES>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)S::TOTAL);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_tc)");
         attr_set = true;
     }
     int *counters = nullptr;
     float *ws = nullptr;
-    if (pl.splits > 1) {
+    if (has_split_tiles(pl)) {
         counters = static_cast<int *>(p->workspace);
         ws = reinterpret_cast<float *>(static_cast<char *>(p->workspace) + kWsCounterBytes);
     }
-    dim3 grid(pl.grid_n, pl.splits, pl.grid_m);
-    kern<<<grid, TC_THREADS, S::TOTAL, st>>>(mw, mx, static_cast<T *>(p->c), p->ldc,
-                                             static_cast<const T *>(p->r), p->ldr, p->M, p->N,
-                                             p->K, pl.kb_per_split, pl.splits, ws, counters);
-    FDPP_CHECK_LAUNCH("gemm_tc_kernel");
+    cudaError_t e = launch_kernel(kern, dim3(pl.grid), dim3(TC_THREADS), S::TOTAL, st, mw, mx,
+                                  static_cast<T *>(p->c), p->ldc, static_cast<const T *>(p->r),
+                                  p->ldr, p->M, p->N, pl.wk, ws, counters);
+    if (e != cudaSuccess) return cuda_status(e, "gemm_tc_kernel launch");
     return FDPP_OK;
 }
 
@@ -440,10 +754,12 @@ template <typename T, int BX, bool SWAP>
 static fdpp_status dispatch_stages(const fdpp_gemm_params *p, const TcPlan &pl,
                                    const CUtensorMap &mw, const CUtensorMap &mx, cudaStream_t st) {
     constexpr int BW = 128;
-    // deep ring: as many stages as fit ~200 KB of shared memory
-    constexpr int DEEP = (200 * 1024) / ((BW + BX) * TC_BK * 2) > 12
-                             ? 12
-                             : (200 * 1024) / ((BW + BX) * TC_BK * 2);
+    // default ring: ~100 KB of stages (>= 4x the ~20 KB/SM Little's-law need
+    // at 6.5 TB/s), small enough that the next kernel's CTA fits beside it on
+    // the SM while this one drains (PDL overlap)
+    constexpr int DEEP = (100 * 1024) / ((BW + BX) * TC_BK * 2) < 4
+                             ? 4
+                             : (100 * 1024) / ((BW + BX) * TC_BK * 2);
     switch (pl.stages) {
         case 1: return launch_tc<T, BW, BX, SWAP, 1>(p, pl, mw, mx, st);
         case 2: return launch_tc<T, BW, BX, SWAP, 2>(p, pl, mw, mx, st);
@@ -496,10 +812,11 @@ static fdpp_status launch_gemv(const fdpp_gemm_params *p, cudaStream_t st) {
     const T *W = static_cast<const T *>(p->w);
     T *C = static_cast<T *>(p->c);
     const T *R = static_cast<const T *>(p->r);
+    cudaError_t err = cudaSuccess;
 #define FDPP_GEMV_CASE(MR)                                                                   \
     case MR:                                                                                 \
-        gemv_kernel<T, MR><<<grid, GEMV_WARPS * 32, 0, st>>>(A, p->lda, W, p->ldw, C, p->ldc, \
-                                                             R, p->ldr, p->M, p->N, p->K);   \
+        err = launch_kernel(gemv_kernel<T, MR>, grid, dim3(GEMV_WARPS * 32), 0, st, A, p->lda, \
+                            W, p->ldw, C, p->ldc, R, p->ldr, p->M, p->N, p->K);              \
         break;
     switch (p->M) {
         FDPP_GEMV_CASE(1)
@@ -513,13 +830,24 @@ static fdpp_status launch_gemv(const fdpp_gemm_params *p, cudaStream_t st) {
         default: break;
     }
 #undef FDPP_GEMV_CASE
-    FDPP_CHECK_LAUNCH("gemv_kernel");
+    if (err != cudaSuccess) return cuda_status(err, "gemv_kernel launch");
     return FDPP_OK;
 }
 
 }  // namespace fdpp
 
 using namespace fdpp;
+
+#ifdef FDPP_TRACE
+extern "C" int fdpp_trace_read(unsigned long long *host, int n) {
+    (void)n;
+    return (int)cudaMemcpyFromSymbol(host, fdpp::g_fdpp_trace, sizeof(fdpp::g_fdpp_trace));
+}
+extern "C" int fdpp_trace_reset(void) {
+    unsigned int z[512] = {0};
+    return (int)cudaMemcpyToSymbol(fdpp::g_fdpp_launch, z, sizeof(z));
+}
+#endif
 
 extern "C" fdpp_status fdpp_prepack_weight(const void *b_kn, void *w_nk, int32_t K, int32_t N,
                                            int64_t ldw, int32_t dtype, void *stream) {

@@ -6,6 +6,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <atomic>
 #include <mutex>
 
 #include "../../include/fdpp.h"
@@ -25,6 +26,9 @@ fdpp_status cuda_status(cudaError_t e, const char *what) {
     set_error("%s: %s", what, cudaGetErrorString(e));
     return FDPP_ERR_CUDA;
 }
+
+static std::atomic<int> g_pdl{1};
+bool pdl_enabled() { return g_pdl.load(std::memory_order_relaxed) != 0; }
 
 int sm_count() {
     static int cached = 0;
@@ -46,7 +50,11 @@ int sm_count() {
 
 extern "C" const char *fdpp_last_error(void) { return fdpp::g_err; }
 
-extern "C" int fdpp_version(void) { return 100; }
+extern "C" int fdpp_version(void) { return 101; }
+
+extern "C" int fdpp_set_pdl(int enable) {
+    return fdpp::g_pdl.exchange(enable ? 1 : 0);
+}
 
 extern "C" int fdpp_sm_count(void) { return fdpp::sm_count(); }
 

@@ -12,7 +12,7 @@ a 2-stage TMA ring (else 1 stage, the single-buffer schedule); ``m_pad`` -> the
 token tile (rounded up to 16/32/64, the legal MMA N sizes); ``b_n`` / ``b_k``
 are CPU cache-blocking parameters with no device meaning (the device tile is
 128 x 64, one SWIZZLE_128B atom wide).  ``flat_gemm_b200`` exposes the
-device knobs directly (token tile, split-K, ring depth).
+device knobs directly (token tile, persistent grid, ring depth).
 """
 
 from __future__ import annotations
@@ -132,8 +132,9 @@ def flat_gemm(a, b, cfg: TileConfig, record_events=None):
     return _g.reference_call(_g.IMPL_B, a, b, block_x=bx, stages=stages)
 
 
-def flat_gemm_b200(a, b, *, block_x: int = 0, splits: int = 0, stages: int = 0, out=None,
+def flat_gemm_b200(a, b, *, block_x: int = 0, ctas: int = 0, stages: int = 0, out=None,
                    residual=None, stream=None):
-    """ImplB with the device knobs exposed (0 = auto)."""
-    return _g.reference_call(_g.IMPL_B, a, b, block_x=block_x, splits=splits, stages=stages,
+    """ImplB with the device knobs exposed (0 = auto): token tile, persistent
+    grid size (stream-K CTAs), ring depth."""
+    return _g.reference_call(_g.IMPL_B, a, b, block_x=block_x, ctas=ctas, stages=stages,
                              out=out, residual=residual, stream=stream)

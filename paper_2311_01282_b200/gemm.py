@@ -110,7 +110,7 @@ def as_activation(a, dtype):
     return a
 
 
-def gemm_params(a, pw: PackedWeight, out, residual=None, block_x=0, splits=0, stages=0):
+def gemm_params(a, pw: PackedWeight, out, residual=None, block_x=0, ctas=0, stages=0):
     prm = _lib.GemmParams()
     prm.a, prm.lda = a.data_ptr(), a.stride(0)
     prm.w, prm.ldw = pw.w.data_ptr(), pw.ldw
@@ -119,11 +119,11 @@ def gemm_params(a, pw: PackedWeight, out, residual=None, block_x=0, splits=0, st
         prm.r, prm.ldr = residual.data_ptr(), residual.stride(0)
     prm.M, prm.N, prm.K = a.shape[0], pw.N, pw.ldw  # zero-padded K contributes exactly 0
     prm.dtype = _lib.dtype_code(a.dtype)
-    prm.block_x, prm.splits, prm.stages = int(block_x), int(splits), int(stages)
+    prm.block_x, prm.ctas, prm.stages = int(block_x), int(ctas), int(stages)
     return prm
 
 
-def run(impl: int, a, pw: PackedWeight, *, out=None, residual=None, block_x=0, splits=0,
+def run(impl: int, a, pw: PackedWeight, *, out=None, residual=None, block_x=0, ctas=0,
         stages=0, stream=None, ws_tag="gemm"):
     """Launch ImplA/B/C on device operands; returns out [M, N]."""
     torch = _torch()
@@ -133,7 +133,7 @@ def run(impl: int, a, pw: PackedWeight, *, out=None, residual=None, block_x=0, s
         raise ValueError(f"activation dtype {a.dtype} != weight dtype {pw.dtype}")
     if out is None:
         out = torch.empty((a.shape[0], pw.N), dtype=a.dtype, device=a.device)
-    prm = gemm_params(a, pw, out, residual, block_x, splits, stages)
+    prm = gemm_params(a, pw, out, residual, block_x, ctas, stages)
     lib = _lib.load()
     need = ctypes.c_size_t()
     _lib.check(lib.fdpp_gemm_workspace_size(impl, ctypes.byref(prm), ctypes.byref(need)), "gemm")

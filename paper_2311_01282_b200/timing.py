@@ -22,17 +22,29 @@ def median_mad(samples):
 
 
 def l2_flush(device=None, nbytes: int = 256 << 20):
-    """Overwrite a buffer twice the 126 MB L2 so the next kernel starts cold."""
+    """READ a buffer twice the 126 MB L2 so the next kernel starts cold.
+
+    A read (not a memset) leaves L2 holding clean lines, as it would after
+    the previous layer's weight stream; a write-flush would make the timed
+    kernel pay for writing back ~126 MB of dirty lines."""
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-    buf = _FLUSH.get(dev.index)
-    if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-        _FLUSH[dev.index] = buf
-    buf.zero_()
+    ent = _FLUSH.get(dev.index)
+    if ent is None or ent[0].numel() * 4 < nbytes:
+        ent = (torch.ones(nbytes // 4, dtype=torch.float32, device=dev),
+               torch.empty((), dtype=torch.float32, device=dev))
+        _FLUSH[dev.index] = ent
+    torch.sum(ent[0], dim=0, out=ent[1])
+
+
+SPIN_CYCLES = 400_000   # ~0.2-0.3 ms at B200 clocks: longer than any host launch path
 
 
 def measure(fn, reps: int, warmup: int = 2, flush_l2: bool = True):
-    """Seconds per call of fn(), one CUDA-event pair per rep, after warmup."""
+    """Seconds per call of fn(), one CUDA-event pair per rep, after warmup.
+
+    Before each rep the stream is parked on a spin kernel, so fn()'s launches
+    are already queued when the start event fires: the host launch latency
+    (Python -> ctypes -> libfdpp) never leaks into the device-timed window."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
@@ -41,6 +53,7 @@ def measure(fn, reps: int, warmup: int = 2, flush_l2: bool = True):
     for _ in range(reps):
         if flush_l2:
             l2_flush()
+        torch.cuda._sleep(SPIN_CYCLES)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)

@@ -83,14 +83,16 @@ def test_ring_depth_is_bit_identical(fd, torch):
     D = __import__("importlib").import_module("paper_2311_01282_b200.dispatch")
     a, b = _operands(torch, 24, 4096, 4096, 7, torch.float16)
     pw = fd.pack_weight(b)
-    base = D.run_device(D.KernelChoice.IMPL_B, a, pw, stages=1, splits=2)
-    for st in (2, 4, 0):
-        assert torch.equal(base, D.run_device(D.KernelChoice.IMPL_B, a, pw, stages=st, splits=2))
-    # rerun determinism with split-K (fixed-order reduction)
-    for sp in (1, 3, 8):
-        x = D.run_device(D.KernelChoice.IMPL_B, a, pw, splits=sp)
-        y = D.run_device(D.KernelChoice.IMPL_B, a, pw, splits=sp)
+    for ctas in (0, 7, 50, -3, -8):   # stream-K fixup (>0) and cluster split-K (<0) paths
+        base = D.run_device(D.KernelChoice.IMPL_B, a, pw, stages=1, ctas=ctas)
+        for st in (2, 4, 0):
+            assert torch.equal(base, D.run_device(D.KernelChoice.IMPL_B, a, pw, stages=st, ctas=ctas))
+    # rerun determinism (stream-K fixup in fixed segment order)
+    for ctas in (1, 3, 148, 300, -1, -2, -5, -8):
+        x = D.run_device(D.KernelChoice.IMPL_B, a, pw, ctas=ctas)
+        y = D.run_device(D.KernelChoice.IMPL_B, a, pw, ctas=ctas)
         assert torch.equal(x, y)
+        assert fd.rel_error_rowwise(x.float().cpu().numpy(), _oracle(a, b)) <= TOL
 
 
 def test_padding_transparency(fd, torch):
