@@ -227,10 +227,10 @@ def decide(m_sweep, med_a, med_b, med_c):
     return m1.value, m2.value
 
 
-def _time_impl(fn, reps, warmup, context):
+def _time_impl(fn, reps, warmup, context, inner=1):
     """3 attempts, accept when MAD <= 0.2 * median (dispatch.py:268-275)."""
     for _ in range(3):
-        samples = measure(fn, reps=reps, warmup=warmup)
+        samples = measure(fn, reps=reps, warmup=warmup, inner=inner)
         med, mad = median_mad(samples)
         if med == 0.0 or mad <= 0.2 * med:
             return med, mad
@@ -252,24 +252,36 @@ def profile_shape(n: int, k: int, m_sweep=DEFAULT_M_SWEEP, reps: int = DEFAULT_R
         raise ValueError("reps must be >= 3")
     names = [c.value for c in KernelChoice]
     medians = {name: [] for name in names}
-    pw = None
+    pws = None
     if timers is None:
         import torch
         _lib.require_cuda()
         dtype = dtype or torch.float16
         g = torch.Generator(device="cuda").manual_seed(seed)
-        b = (torch.randn((k, n), generator=g, device="cuda") / np.sqrt(k)).to(dtype)
-        pw = _g.pack_weight(b, dtype)
-        del b
+        # enough weight copies that one timed batch streams >= 2x the 126 MB L2
+        nbytes = n * k * 2
+        nrot = max(1, min(16, -(-(256 << 20) // nbytes)))
+        pws = []
+        for _ in range(nrot):
+            b = (torch.randn((k, n), generator=g, device="cuda") / np.sqrt(k)).to(dtype)
+            pws.append(_g.pack_weight(b, dtype))
+            del b
     for m in m_sweep:
         point = {"m": m}
         if timers is None:
-            a = torch.randn((m, pw.ldw), generator=g, device="cuda").to(dtype)
+            a = torch.randn((m, pws[0].ldw), generator=g, device="cuda").to(dtype)
             out = torch.empty((m, n), dtype=dtype, device="cuda")
+            rot = [0]
+
+            def mk(choice):
+                def f():
+                    run_device(choice, a, pws[rot[0] % len(pws)], out=out)
+                    rot[0] += 1
+                return f
             runs = {
-                "ImplA": (lambda: run_device(KernelChoice.IMPL_A, a, pw, out=out)) if m <= GEMV_MAX_M else None,
-                "ImplB": lambda: run_device(KernelChoice.IMPL_B, a, pw, out=out),
-                "ImplC": lambda: run_device(KernelChoice.IMPL_C, a, pw, out=out),
+                "ImplA": mk(KernelChoice.IMPL_A) if m <= GEMV_MAX_M else None,
+                "ImplB": mk(KernelChoice.IMPL_B),
+                "ImplC": mk(KernelChoice.IMPL_C),
             }
         for name in names:
             if timers is not None:
@@ -277,7 +289,8 @@ def profile_shape(n: int, k: int, m_sweep=DEFAULT_M_SWEEP, reps: int = DEFAULT_R
             elif runs[name] is None:
                 med, mad = float("inf"), 0.0
             else:
-                med, mad = _time_impl(runs[name], reps, warmup, f"{name} at M={m} [N={n}, K={k}]")
+                med, mad = _time_impl(runs[name], reps, warmup, f"{name} at M={m} [N={n}, K={k}]",
+                                      inner=len(pws))
             medians[name].append(med)
             point[name] = med
             point[f"{name}_mad"] = mad

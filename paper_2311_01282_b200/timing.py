@@ -39,12 +39,16 @@ def l2_flush(device=None, nbytes: int = 256 << 20):
 SPIN_CYCLES = 400_000   # ~0.2-0.3 ms at B200 clocks: longer than any host launch path
 
 
-def measure(fn, reps: int, warmup: int = 2, flush_l2: bool = True):
+def measure(fn, reps: int, warmup: int = 2, flush_l2: bool = True, inner: int = 1):
     """Seconds per call of fn(), one CUDA-event pair per rep, after warmup.
 
     Before each rep the stream is parked on a spin kernel, so fn()'s launches
     are already queued when the start event fires: the host launch latency
-    (Python -> ctypes -> libfdpp) never leaks into the device-timed window."""
+    (Python -> ctypes -> libfdpp) never leaks into the device-timed window.
+    ``inner`` > 1 times that many back-to-back calls per rep and divides (the
+    event clock ticks in ~2 us steps on this part; a longer window resolves
+    sub-tick differences).  Callers that pass inner > 1 must rotate operands
+    so consecutive calls do not hit in L2."""
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
@@ -57,8 +61,9 @@ def measure(fn, reps: int, warmup: int = 2, flush_l2: bool = True):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        fn()
+        for _ in range(inner):
+            fn()
         e1.record(stream)
         e1.synchronize()
-        out.append(e0.elapsed_time(e1) * 1e-3)
+        out.append(e0.elapsed_time(e1) * 1e-3 / inner)
     return out

@@ -1,0 +1,39 @@
+"""Summarise an `ncu --set full` report (.ncu-rep) into text for profiles/."""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+    "launch__shared_mem_per_block_dynamic", "launch__occupancy_limit_shared_mem",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__waves_per_multiprocessor",
+    "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
+    "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second",
+]
+
+
+def main(path):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        print("kernel:", r[hdr.index("Kernel Name")][:120])
+        for k in KEYS:
+            if k in hdr:
+                i = hdr.index(k)
+                print(f"  {k:70s} {r[i]:>16s} {units[i]}")
+        st = [(hdr[i], float(r[i].replace(",", "") or 0)) for i in range(len(hdr))
+              if hdr[i].startswith("smsp__average_warps_issue_stalled") and hdr[i].endswith("_per_issue_active.ratio")]
+        st.sort(key=lambda x: -x[1])
+        print("  top stall reasons (warps per issue):")
+        for name, v in st[:8]:
+            print(f"    {name.replace('smsp__average_warps_issue_stalled_', '').replace('_per_issue_active.ratio', ''):30s} {v:6.2f}")
+        print()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
