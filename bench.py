@@ -256,20 +256,51 @@ def run_gpu(args):
     ops["attention_async(+recompute)"] = {"s_per_launch": t_attn, "bytes": attn_bytes,
                                           "launches_per_step": dec.n_layers}
     shapes = cfg.gemm_shapes()
-    bufs = {"qkv": (dec.h, dec.qkv), "o": (dec.attn.view(B, hq * dh), dec.h),
-            "gate_up": (dec.h, dec.gu), "down": (dec.act, dec.h), "lm_head": (dec.h, dec.logits)}
-    for op in ("qkv", "o", "gate_up", "down", "lm_head"):
-        a, out = bufs[op]
-        ws = [Ld[op] for Ld in dec.layers] if op != "lm_head" else [dec.lm_head]
-        ch = dec.choices[op]
-
-        def run_all(a=a, out=out, ws=ws, ch=ch):
-            for w in ws:
-                D.run_device(ch, a, w, out=out, ws_tag="decode_gemm")
-        t = _op_graph_time(torch, run_all, reps) / len(ws)
-        n, k = shapes[op]
-        ops[f"gemm_{op}[{n}x{k}]:{ch.value}"] = {"s_per_launch": t, "bytes": n * k * 2 + B * k * 2 + B * n * 2,
-                                                 "launches_per_step": len(ws)}
+    from paper_2311_01282_b200.gemm import run_fused
+    gb = lambda n, k: n * k * 2 + B * k * 2 + B * n * 2  # noqa: E731
+    if dec.fused:
+        L0 = dec.layers
+        per_op = {
+            f"gemm_qkv+rmsnorm+rope[{shapes['qkv'][0]}x{shapes['qkv'][1]}]:ImplB": (
+                lambda: [run_fused(dec.x, Ld["qkv_f"], x_op=3, ssq_in=dec.ssq_a, ssq_tiles=dec.ssq_tiles,
+                                   eps=cfg.eps, ws_tag="decode_gemm",
+                                   rope={"q_out": dec.q, "k_cache": dec.k_cache[i],
+                                         "v_cache": dec.v_cache[i], "pos": dec.pos,
+                                         "theta": cfg.rope_theta}) for i, Ld in enumerate(L0)],
+                gb(*shapes["qkv"]), len(L0)),
+            f"gemm_o+residual+ssq[{shapes['o'][0]}x{shapes['o'][1]}]:ImplB": (
+                lambda: [run_fused(dec.attn.view(B, hq * dh), Ld["o"], out=dec.h, residual=dec.x,
+                                   ssq_out=dec.ssq_b, ws_tag="decode_gemm") for Ld in L0],
+                gb(*shapes["o"]), len(L0)),
+            f"gemm_gate_up+rmsnorm[{shapes['gate_up'][0]}x{shapes['gate_up'][1]}]:ImplB": (
+                lambda: [run_fused(dec.x, Ld["gate_up_f"], out=dec.gu, x_op=3, ssq_in=dec.ssq_b,
+                                   ssq_tiles=dec.ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
+                         for Ld in L0],
+                gb(*shapes["gate_up"]), len(L0)),
+            f"gemm_down+residual+ssq[{shapes['down'][0]}x{shapes['down'][1]}]:ImplB": (
+                lambda: [run_fused(dec.act, Ld["down"], out=dec.h, residual=dec.x,
+                                   ssq_out=dec.ssq_a, ws_tag="decode_gemm") for Ld in L0],
+                gb(*shapes["down"]), len(L0)),
+            f"gemm_lm_head+rmsnorm[{shapes['lm_head'][0]}x{shapes['lm_head'][1]}]:ImplB": (
+                lambda: run_fused(dec.x, dec.lm_head_f, out=dec.logits, x_op=3, ssq_in=dec.ssq_a,
+                                  ssq_tiles=dec.ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm"),
+                gb(*shapes["lm_head"]), 1),
+        }
+    else:
+        bufs = {"qkv": (dec.h, dec.qkv), "o": (dec.attn.view(B, hq * dh), dec.h),
+                "gate_up": (dec.h, dec.gu), "down": (dec.act, dec.h), "lm_head": (dec.h, dec.logits)}
+        per_op = {}
+        for op in ("qkv", "o", "gate_up", "down", "lm_head"):
+            a, out = bufs[op]
+            ws = [Ld[op] for Ld in dec.layers] if op != "lm_head" else [dec.lm_head]
+            ch = dec.choices[op]
+            n, k = shapes[op]
+            per_op[f"gemm_{op}[{n}x{k}]:{ch.value}"] = (
+                lambda a=a, out=out, ws=ws, ch=ch: [D.run_device(ch, a, w, out=out, ws_tag="decode_gemm")
+                                                    for w in ws], gb(n, k), len(ws))
+    for name, (fn, byt, nl) in per_op.items():
+        t = _op_graph_time(torch, fn, reps) / nl
+        ops[name] = {"s_per_launch": t, "bytes": byt, "launches_per_step": nl}
     peak, peak_kind = _peaks()
     for name, o in ops.items():
         o["gbs"] = o["bytes"] / o["s_per_launch"] / 1e9

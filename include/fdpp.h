@@ -147,6 +147,35 @@ fdpp_status fdpp_impl_c_gemm(const fdpp_gemm_params *p, void *stream);
 /* run_kernel(choice, a, b) (dispatch.py:155-156). */
 fdpp_status fdpp_run_kernel(int32_t impl, const fdpp_gemm_params *p, void *stream);
 
+/* Fusions around the ImplB flat GEMM for the decode step (the caller of the
+ * path): prologue transforms of each landed activation tile, and
+ * epilogues that replace the standalone glue kernels. */
+typedef struct fdpp_gemm_fuse {
+    int32_t x_op;            /* 0 none; 1 A <- RMSNorm(A) * norm_w (row sums of squares
+                                given as ssq_in[ssq_tiles][ssq_ld]); 2 A <- silu(A[:, :K]) *
+                                A[:, K:2K] (lda >= 2K); 3 folded RMSNorm: the norm weight is
+                                pre-multiplied into W's columns and each output row is
+                                scaled by its inverse RMS in the epilogue (from ssq_in)    */
+    const float *ssq_in;
+    int32_t ssq_tiles, ssq_ld;
+    const void *norm_w;      /* [K] RMSNorm weight, dtype                              */
+    float eps;
+    float *ssq_out;          /* optional [N/128][ssq_out_ld]: sum of squares of each
+                                stored output row over every 128-column tile            */
+    int32_t ssq_out_ld;
+    void *q_out;             /* optional RoPE + KV append (QKV projection, head dim 128,
+                                N = (Hq + 2 Hkv) * 128): q -> q_out [M, Hq, 128],
+                                k/v -> caches [M, Hkv, Lmax, 128] at row pos[m]; C unused */
+    void *k_cache, *v_cache;
+    const int32_t *pos;
+    int32_t Hq, Hkv;
+    int64_t cache_stride_b, cache_stride_h;
+    float theta;
+} fdpp_gemm_fuse;
+
+/* ImplB with the fusions above (fused epilogues run in cluster split-K mode). */
+fdpp_status fdpp_gemm_fused(const fdpp_gemm_params *p, const fdpp_gemm_fuse *fuse, void *stream);
+
 /* ------------------------------------------ subsystem 3: heuristic dispatch */
 /* dispatch(m, n, k, table) on one entry (dispatch.py:189-197): 0=A,1=B,2=C. */
 int32_t fdpp_dispatch_choose(int32_t m, int32_t m1, int32_t m2);
@@ -174,9 +203,10 @@ fdpp_status fdpp_rope_append(const void *qkv, void *q_out, void *k_cache, void *
 /* out[r, j] = silu(gu[r, j]) * gu[r, F + j] for a fused [rows, 2F] gate/up. */
 fdpp_status fdpp_silu_mul(const void *gu, void *out, int32_t rows, int32_t F, int32_t dtype,
                           void *stream);
-/* out[b, :] = table[ids[b], :]. */
+/* out[b, :] = table[ids[b], :]; optional ssq_out[b] = sum_j out[b, j]^2 (the
+ * one-tile row sums a fused RMSNorm prologue consumes). */
 fdpp_status fdpp_embed(const int32_t *ids, const void *table, void *out, int32_t B, int32_t dim,
-                       int32_t dtype, void *stream);
+                       float *ssq_out, int32_t dtype, void *stream);
 /* ids[r] = argmax_j logits[r, j] (lowest index on ties). */
 fdpp_status fdpp_argmax(const void *logits, int32_t *ids, int32_t rows, int32_t vocab,
                         int32_t dtype, void *stream);

@@ -49,6 +49,17 @@ class GemmParams(ctypes.Structure):
     ]
 
 
+class GemmFuse(ctypes.Structure):
+    """fdpp_gemm_fuse (include/fdpp.h)."""
+    _fields_ = [
+        ("x_op", c_i32), ("ssq_in", c_vp), ("ssq_tiles", c_i32), ("ssq_ld", c_i32),
+        ("norm_w", c_vp), ("eps", c_f32), ("ssq_out", c_vp), ("ssq_out_ld", c_i32),
+        ("q_out", c_vp), ("k_cache", c_vp), ("v_cache", c_vp), ("pos", c_vp),
+        ("Hq", c_i32), ("Hkv", c_i32), ("cache_stride_b", c_i64), ("cache_stride_h", c_i64),
+        ("theta", c_f32),
+    ]
+
+
 # name -> (restype, argtypes); must cover every function declared in include/fdpp.h
 SIGNATURES = {
     "fdpp_last_error": (ctypes.c_char_p, []),
@@ -64,6 +75,7 @@ SIGNATURES = {
     "fdpp_impl_b_flat": (c_i32, [ctypes.POINTER(GemmParams), c_vp]),
     "fdpp_impl_c_gemm": (c_i32, [ctypes.POINTER(GemmParams), c_vp]),
     "fdpp_run_kernel": (c_i32, [c_i32, ctypes.POINTER(GemmParams), c_vp]),
+    "fdpp_gemm_fused": (c_i32, [ctypes.POINTER(GemmParams), ctypes.POINTER(GemmFuse), c_vp]),
     "fdpp_dispatch_choose": (c_i32, [c_i32, c_i32, c_i32]),
     "fdpp_first_sustained": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), c_i32, c_i32]),
     "fdpp_profile_decide": (c_i32, [ctypes.POINTER(c_i32), ctypes.POINTER(ctypes.c_double),
@@ -74,7 +86,7 @@ SIGNATURES = {
     "fdpp_rope_append": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32,
                                  c_i64, c_i64, c_f32, c_i32, c_vp]),
     "fdpp_silu_mul": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
-    "fdpp_embed": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
+    "fdpp_embed": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_i32, c_vp]),
     "fdpp_argmax": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_advance_positions": (c_i32, [c_vp, c_vp, c_i32, c_vp]),
 }

@@ -78,18 +78,35 @@ __global__ void silu_mul_kernel(const T *__restrict__ gu, T *__restrict__ out, i
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
         const float g = Elem<T>::to_f(gu[(int64_t)r * 2 * F + j]);
         const float u = Elem<T>::to_f(gu[(int64_t)r * 2 * F + F + j]);
-        out[(int64_t)r * F + j] = Elem<T>::from_f(g / (1.f + __expf(-g)) * u);
+        out[(int64_t)r * F + j] = Elem<T>::from_f(__fdividef(g, 1.f + __expf(-g)) * u);
     }
 }
 
 template <typename T>
 __global__ void embed_kernel(const int32_t *__restrict__ ids, const T *__restrict__ table,
-                             T *__restrict__ out, int dim) {
+                             T *__restrict__ out, int dim, float *ssq_out) {
     pdl_wait();
     pdl_trigger();
     const int b = blockIdx.x;
     const int64_t id = ids[b];
-    for (int i = threadIdx.x; i < dim; i += blockDim.x) out[(int64_t)b * dim + i] = table[id * dim + i];
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
+        const T v = table[id * dim + i];
+        out[(int64_t)b * dim + i] = v;
+        const float f = Elem<T>::to_f(v);
+        ss = fmaf(f, f, ss);
+    }
+    if (ssq_out) {
+        __shared__ float red[32];
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float t = 0.f;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+            ssq_out[b] = t;
+        }
+    }
 }
 
 template <typename T>
@@ -182,13 +199,13 @@ extern "C" fdpp_status fdpp_silu_mul(const void *gu, void *out, int32_t rows, in
 }
 
 extern "C" fdpp_status fdpp_embed(const int32_t *ids, const void *table, void *out, int32_t B,
-                                  int32_t dim, int32_t dtype, void *stream) {
+                                  int32_t dim, float *ssq_out, int32_t dtype, void *stream) {
     FDPP_REQUIRE(B >= 1 && dim >= 1, FDPP_ERR_SHAPE, "embed dims");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSuccess;
     FDPP_DT_SWITCH(dtype, e = launch_kernel(embed_kernel<T>, dim3(B), dim3(256), 0, st, ids,
                                             static_cast<const T *>(table), static_cast<T *>(out),
-                                            (int)dim));
+                                            (int)dim, ssq_out));
     if (e != cudaSuccess) return cuda_status(e, "embed_kernel launch");
     return FDPP_OK;
 }

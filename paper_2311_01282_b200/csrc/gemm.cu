@@ -16,6 +16,7 @@
 //                             the MMA M axis (128-row tiles), weights on N.
 //
 // All paths: C[M,N] = A[M,K] · W[N,K]^T (+ R), W = prepacked reference B[K,N].
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -136,17 +137,40 @@ gemv_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W, int64
 //               the whole K of its tile is written straight to C (+ residual);
 //               a tile split across CTAs deposits fp32 partials and the last
 //               arriving CTA (atomic ticket) sums them in fixed segment order,
-//               so results are bitwise reproducible for a given grid.
+//               so results are bitwise reproducible for a given grid;
+//   warp 6      (XF kernels only) activation transform: applies a fused
+//               RMSNorm or SiLU(gate)*up to each landed activation tile in
+//               shared memory before releasing it to the MMA.
 constexpr int TC_BK = 64;  // 64 fp16 = 128 B rows: one SWIZZLE_128B atom wide
 constexpr int TC_THREADS = 192;
+constexpr int XF_WARPS = 2;                        // activation-transform warps 6..7
+constexpr int TC_THREADS_XF = TC_THREADS + 32 * XF_WARPS;
+constexpr int XF_MAX_M = 256;
 
-template <int BW, int BX, int STAGES>
+// Fusions around the flat GEMM (mirrors fdpp_gemm_fuse in include/fdpp.h).
+struct GemmFuse {
+    int x_op;                       // 0 none, 1 RMSNorm(x) * w, 2 silu(x) * up
+    const float *ssq_in;
+    int ssq_tiles, ssq_ld;
+    const void *norm_w;
+    float eps;
+    float *ssq_out;                 // epilogue: per-(n-tile, row) sum of squares of the output
+    int ssq_out_ld;
+    void *q_out, *k_cache, *v_cache;  // epilogue: RoPE + KV append (QKV projection)
+    const int32_t *pos;
+    int Hq, Hkv;
+    int64_t cache_sb, cache_sh;
+    float theta;
+};
+
+template <int BW, int BX, int STAGES, bool XF = false>
 struct TcSmem {
     static constexpr uint32_t W_BYTES = BW * TC_BK * 2;
     static constexpr uint32_t X_BYTES = BX * TC_BK * 2;
-    static constexpr uint32_t STAGE_BYTES = W_BYTES + X_BYTES;
-    static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
-    static constexpr uint32_t TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
+    static constexpr uint32_t STAGE_BYTES = W_BYTES + X_BYTES + (XF ? X_BYTES : 0);
+    static constexpr uint32_t RING = STAGES * STAGE_BYTES;
+    static constexpr uint32_t BAR_OFF = RING;
+    static constexpr uint32_t TOTAL = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;  // + align slack
 };
 
 struct TcWork {
@@ -158,25 +182,174 @@ struct TcWork {
 template <typename T, int BW, bool SWAP>
 __device__ __forceinline__ void epi_store16(const float (&v)[16], T *C, int64_t ldc, const T *R,
                                             int64_t ldr, int M, int N, int n0, int m0, int row,
-                                            int c0) {
+                                            int c0, const float *row_scale) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         const int n = SWAP ? n0 + row : n0 + c0 + j;
         const int m = SWAP ? m0 + c0 + j : m0 + row;
         if (n < N && m < M) {
             float o = v[j];
+            if (row_scale) o *= row_scale[m];  // folded RMSNorm: inverse RMS of token m
             if (R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
             C[(int64_t)m * ldc + n] = Elem<T>::from_f(o);
         }
     }
 }
 
-template <typename T, int BW, int BX, bool SWAP, int STAGES>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// Inverse RMS of rows [0, M) from the per-tile sums of squares the previous
+// residual GEMM's epilogue wrote (fixed tile order; 8 loads in flight).
+__device__ __forceinline__ void inv_rms_rows(float *dst, int M, int K, const GemmFuse &fz, int tid,
+                                             int nthreads) {
+    for (int r = tid; r < M && r < XF_MAX_M; r += nthreads) {
+        float ss = 0.f;
+        for (int t0 = 0; t0 < fz.ssq_tiles; t0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                v[q] = t0 + q < fz.ssq_tiles ? __ldcg(&fz.ssq_in[(int64_t)(t0 + q) * fz.ssq_ld + r]) : 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ss += v[q];
+        }
+        dst[r] = rsqrtf(ss / K + fz.eps);
+    }
+}
+
+// TMA producer shared by both kernels.  coord(i, kb, n_row, m_row) maps the
+// i-th k-block of this CTA to its tile coordinates.  With XF the activation
+// (and SiLU's "up") tiles complete on xfull[s]; full[s] then also waits for
+// the transform warp's arrive.
+template <typename S, int STAGES, bool XF, typename Coord>
+__device__ __forceinline__ void tc_produce(uint8_t *smem, uint64_t *full, uint64_t *empty,
+                                           uint64_t *xfull, const CUtensorMap *tmW,
+                                           const CUtensorMap *tmX, const CUtensorMap *tmU,
+                                           bool with_up, int n, Coord coord) {
+    constexpr uint32_t WB = S::W_BYTES, XB = S::X_BYTES;
+    const uint32_t xbytes = XB * (with_up ? 2 : 1);
+    auto load_x = [&](int i, int s) {
+        int kb, nr, mr;
+        coord(i, kb, nr, mr);
+        uint8_t *sx = smem + s * S::STAGE_BYTES + WB;
+        uint64_t *bar = XF ? &xfull[s] : &full[s];
+        if (XF) mbar_arrive_expect_tx(bar, xbytes);
+        tma_load_2d(sx, tmX, bar, kb * TC_BK, mr, kEvictLast);
+        if (XF && with_up) tma_load_2d(sx + XB, tmU, bar, kb * TC_BK, mr, kEvictLast);
+    };
+    // PDL: weights do not depend on any earlier kernel -- request the first
+    // ring's worth before waiting; activations follow once they are visible.
+    const int pre = min(n, STAGES);
+    for (int i = 0; i < pre; ++i) {
+        int kb, nr, mr;
+        coord(i, kb, nr, mr);
+        mbar_arrive_expect_tx(&full[i], XF ? WB : WB + XB);
+        tma_load_2d(smem + i * S::STAGE_BYTES, tmW, &full[i], kb * TC_BK, nr, kEvictFirst);
+    }
+    pdl_wait();
+    for (int i = 0; i < pre; ++i) load_x(i, i);
+    for (int i = pre; i < n; ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+        int kb, nr, mr;
+        coord(i, kb, nr, mr);
+        mbar_arrive_expect_tx(&full[s], XF ? WB : WB + XB);
+        tma_load_2d(smem + s * S::STAGE_BYTES, tmW, &full[s], kb * TC_BK, nr, kEvictFirst);
+        load_x(i, s);
+    }
+    pdl_trigger();  // every load issued: let the next kernel start its prologue
+}
+
+// Transform warps (XF, warps 6..7): per landed activation tile apply
+// RMSNorm(x)*w (x_op 1; inverse RMS from the producer GEMM's per-tile sums of
+// squares) or silu(gate)*up (x_op 2) in place, in the SWIZZLE_128B layout, then
+// release the stage to the MMA (generic writes -> async-proxy fence -> one
+// arrive per warp).  Rounding matches the standalone rmsnorm / silu_mul kernels.
+template <typename T, typename S, int STAGES, int BX, typename Coord>
+__device__ __forceinline__ void tc_transform(uint8_t *smem, uint64_t *full, uint64_t *xfull,
+                                             float *inv_rms, int M, int K, const GemmFuse &fz,
+                                             int n, Coord coord, int xw, int lane) {
+    constexpr int CH = BX * 8;                           // 16-B chunks per activation tile
+    constexpr int PER = (CH + XF_WARPS * 32 - 1) / (XF_WARPS * 32);
+    const int tid = xw * 32 + lane;
+    pdl_wait();
+    if (fz.x_op == 1) {
+        for (int r = tid; r < M && r < XF_MAX_M; r += XF_WARPS * 32) {
+            float ss = 0.f;
+            for (int t0 = 0; t0 < fz.ssq_tiles; t0 += 8) {  // 8 loads in flight, summed in tile order
+                float v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    v[q] = t0 + q < fz.ssq_tiles ? __ldcg(&fz.ssq_in[(int64_t)(t0 + q) * fz.ssq_ld + r]) : 0.f;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) ss += v[q];
+            }
+            inv_rms[r] = rsqrtf(ss / K + fz.eps);
+        }
+        named_bar_sync(2, XF_WARPS * 32);
+    }
+    const T *w = static_cast<const T *>(fz.norm_w);
+    for (int i = 0; i < n; ++i) {
+        const int s = i % STAGES;
+        int kb, nr, mr;
+        coord(i, kb, nr, mr);
+        // prefetch this stage's norm-weight chunks before waiting for the tile
+        int4 nw[PER];
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int ch = tid + j * XF_WARPS * 32;
+            const int r = ch >> 3, k = kb * TC_BK + ((((ch & 7) ^ (r & 7))) << 3);
+            nw[j] = (fz.x_op == 1 && ch < CH && k < K) ? __ldg(reinterpret_cast<const int4 *>(w + k))
+                                                        : make_int4(0, 0, 0, 0);
+        }
+        mbar_wait(&xfull[s], (i / STAGES) & 1);
+        uint8_t *sx = smem + s * S::STAGE_BYTES + S::W_BYTES;
+        const uint8_t *su = sx + S::X_BYTES;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int ch = tid + j * XF_WARPS * 32;
+            if (ch >= CH) break;
+            const int r = ch >> 3;
+            int4 raw = *reinterpret_cast<int4 *>(sx + ch * 16);
+            uint32_t xv[4] = {(uint32_t)raw.x, (uint32_t)raw.y, (uint32_t)raw.z, (uint32_t)raw.w};
+            uint32_t out[4];
+            if (fz.x_op == 1) {
+                const int m = mr + r;
+                const float inv = m < M ? inv_rms[m] : 0.f;
+                uint32_t nv[4] = {(uint32_t)nw[j].x, (uint32_t)nw[j].y, (uint32_t)nw[j].z, (uint32_t)nw[j].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 x = Elem<T>::to_f2(xv[q]);
+                    const float2 g = Elem<T>::to_f2(nv[q]);
+                    T lo = Elem<T>::from_f(x.x * inv * g.x), hi = Elem<T>::from_f(x.y * inv * g.y);
+                    out[q] = (uint32_t)(*reinterpret_cast<uint16_t *>(&lo)) |
+                             ((uint32_t)(*reinterpret_cast<uint16_t *>(&hi)) << 16);
+                }
+            } else {
+                int4 ur = *reinterpret_cast<const int4 *>(su + ch * 16);
+                uint32_t uv[4] = {(uint32_t)ur.x, (uint32_t)ur.y, (uint32_t)ur.z, (uint32_t)ur.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 g = Elem<T>::to_f2(xv[q]);
+                    const float2 u = Elem<T>::to_f2(uv[q]);
+                    T lo = Elem<T>::from_f(__fdividef(g.x, 1.f + __expf(-g.x)) * u.x);
+                    T hi = Elem<T>::from_f(__fdividef(g.y, 1.f + __expf(-g.y)) * u.y);
+                    out[q] = (uint32_t)(*reinterpret_cast<uint16_t *>(&lo)) |
+                             ((uint32_t)(*reinterpret_cast<uint16_t *>(&hi)) << 16);
+                }
+            }
+            *reinterpret_cast<int4 *>(sx + ch * 16) = make_int4(out[0], out[1], out[2], out[3]);
+        }
+        fence_proxy_async_smem();  // make the generic-proxy writes visible to tcgen05
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+    }
+}
+
+template <typename T, int BW, int BX, bool SWAP, int STAGES, bool XF>
+__global__ void __launch_bounds__(XF ? TC_THREADS_XF : TC_THREADS, XF ? 2 : 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-               T *C, int64_t ldc, const T *R /* may alias C */, int64_t ldr, int M, int N,
-               const TcWork wk, float *__restrict__ ws, int *__restrict__ counters) {
-    using S = TcSmem<BW, BX, STAGES>;
+               const __grid_constant__ CUtensorMap tmU, T *C, int64_t ldc,
+               const T *R /* may alias C */, int64_t ldr, int M, int N, int K, const TcWork wk,
+               float *__restrict__ ws, int *__restrict__ counters, const GemmFuse fz) {
+    using S = TcSmem<BW, BX, STAGES, XF>;
     constexpr int MMA_M = SWAP ? BW : BX;
     constexpr int MMA_N = SWAP ? BX : BW;
     static_assert(MMA_M == 128, "tcgen05 tile uses the 128-lane MMA");
@@ -192,10 +365,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                                                 ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);
     uint64_t *empty = full + STAGES;
-    uint64_t *tmem_full = empty + STAGES;      // [2]
+    uint64_t *xfull = empty + STAGES;
+    uint64_t *tmem_full = xfull + STAGES;      // [2]
     uint64_t *tmem_empty = tmem_full + 2;      // [2]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 2);
     __shared__ int s_is_last;
+    __shared__ float s_inv_rms[XF_MAX_M];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int KB = wk.kb_total;
@@ -218,8 +393,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
         prefetch_tmap(&tmW);
         prefetch_tmap(&tmX);
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], XF ? 1 + XF_WARPS : 1);
             mbar_init(&empty[s], 1);
+            mbar_init(&xfull[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tmem_full[b], 1);
@@ -233,39 +409,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    auto coord = [&](int i, int &kb, int &nr, int &mr) {
+        const int u = u0 + i, t = u / KB;
+        kb = u % KB;
+        nr = (t % wk.n_tiles_n) * BW;
+        mr = (t / wk.n_tiles_n) * BX;
+    };
+
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer over the whole unit range
-            // PDL: the weight stream does not depend on any earlier kernel, so
-            // the first ring's worth of W tiles is requested before waiting on
-            // the predecessor; activation tiles follow once its output is visible.
-            const int pre = min(u1 - u0, STAGES);
-            for (int i = 0; i < pre; ++i) {
-                const int u = u0 + i, t = u / KB, kb = u % KB;
-                mbar_arrive_expect_tx(&full[i], S::STAGE_BYTES);
-                tma_load_2d(smem + i * S::STAGE_BYTES, &tmW, &full[i], kb * TC_BK,
-                            (t % wk.n_tiles_n) * BW, kEvictFirst);
-            }
-            FDPP_TRACE_AT(1);
-            pdl_wait();
-            FDPP_TRACE_AT(2);
-            for (int i = 0; i < pre; ++i) {
-                const int u = u0 + i, t = u / KB, kb = u % KB;
-                tma_load_2d(smem + i * S::STAGE_BYTES + S::W_BYTES, &tmX, &full[i], kb * TC_BK,
-                            (t / wk.n_tiles_n) * BX, kEvictLast);
-            }
-            for (int u = u0 + pre, i = pre; u < u1; ++u, ++i) {
-                const int s = i % STAGES;
-                const uint32_t ph = (i / STAGES) & 1;
-                const int t = u / KB, kb = u % KB;
-                mbar_wait(&empty[s], ph ^ 1);
-                uint8_t *sw = smem + s * S::STAGE_BYTES;
-                mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-                tma_load_2d(sw, &tmW, &full[s], kb * TC_BK, (t % wk.n_tiles_n) * BW, kEvictFirst);
-                tma_load_2d(sw + S::W_BYTES, &tmX, &full[s], kb * TC_BK, (t / wk.n_tiles_n) * BX,
-                            kEvictLast);
-            }
-            pdl_trigger();  // every load issued: let the next kernel start its prologue
-        }
+        if (lane == 0)
+            tc_produce<S, STAGES, XF>(smem, full, empty, xfull, &tmW, &tmX, &tmU, fz.x_op == 2,
+                                      u1 - u0, coord);
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
             int seg = 0;
@@ -299,11 +453,20 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                 }
             }
         }
-    } else {  // ---------------- epilogue warps 2..5
+    } else if (XF && warp >= 6) {
+        tc_transform<T, S, STAGES, BX>(smem, full, xfull, s_inv_rms, M, K, fz, u1 - u0, coord,
+                                       warp - 6, lane);
+    } else if (warp >= 2 && warp <= 5) {  // ---------------- epilogue warps 2..5
         pdl_wait();  // residual / C / workspace belong to the stream's earlier kernels
         const int quad = warp & 3;
         const int row = quad * 32 + lane;  // TMEM lane = accumulator row
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        const float *rscale = nullptr;
+        if (fz.x_op == 3) {  // folded RMSNorm: scale rows in the epilogue
+            inv_rms_rows(s_inv_rms, M, K, fz, threadIdx.x - 64, 128);
+            named_bar_sync(1, 128);
+            rscale = s_inv_rms;
+        }
         int seg = 0;
         for (int u = u0; u < u1; ++seg) {
             const int t = u / KB, kb_start = u % KB;
@@ -329,7 +492,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
                 float v[16];
                 tmem_ld16(tmem_base + buf * ACC_COLS + lane_off + c0, v);
                 if (whole) {
-                    epi_store16<T, BW, SWAP>(v, C, ldc, R, ldr, M, N, n0, m0, row, c0);
+                    epi_store16<T, BW, SWAP>(v, C, ldc, R, ldr, M, N, n0, m0, row, c0, rscale);
                 } else {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)   // partial tile layout [BX m][BW n]
@@ -378,7 +541,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 #pragma unroll
                         for (int j = 0; j < 16; ++j) acc[j] += val[q][j];
                 }
-                epi_store16<T, BW, SWAP>(acc, C, ldc, R, ldr, M, N, n0, m0, row, c0);
+                epi_store16<T, BW, SWAP>(acc, C, ldc, R, ldr, M, N, n0, m0, row, c0, rscale);
             }
         }
     }
@@ -399,39 +562,47 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 // column slice r across ranks 0..CS-1 in fixed order and writes C (+residual)
 // -- so there are no global partials, fences or tickets, and the result is
 // bitwise reproducible.  All CS * n_tiles CTAs are co-resident (one wave).
+// Fused epilogues (GemmFuse): per-(tile, row) sums of squares of the output
+// (feeding the next GEMM's RMSNorm prologue) and RoPE + KV-cache append for the
+// QKV projection (a 128-row weight tile is exactly one head).
 struct TcCluster {
     int n_tiles_n, kb_total, kb_per, cs;
 };
 
-template <int BX, int STAGES>
+template <int BX, int STAGES, bool XF>
 struct ClSmem {
-    using S = TcSmem<128, BX, STAGES>;
+    using S = TcSmem<128, BX, STAGES, XF>;
     static constexpr uint32_t RING = STAGES * S::STAGE_BYTES;
     static constexpr uint32_t PART = BX * 128 * 4;  // fp32 partial [MMA_N][128]
-    static constexpr uint32_t BAR_OFF = RING > PART ? RING : PART;
-    static constexpr uint32_t TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+    static constexpr uint32_t BAR_OFF = RING > 2 * PART ? RING : 2 * PART;  // + RoPE staging
+    static constexpr uint32_t TOTAL = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;
 };
 
-template <typename T, int BX, int STAGES>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+template <typename T, int BX, int STAGES, bool XF>
+__global__ void __launch_bounds__(XF ? TC_THREADS_XF : TC_THREADS, XF ? 2 : 1)
 gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                    T *C, int64_t ldc, const T *R /* may alias C */, int64_t ldr, int M, int N,
-                    const TcCluster ck) {
+                    const __grid_constant__ CUtensorMap tmU, T *C, int64_t ldc,
+                    const T *R /* may alias C */, int64_t ldr, int M, int N, int K,
+                    const TcCluster ck, const GemmFuse fz) {
     constexpr int BW = 128;
-    using S = TcSmem<BW, BX, STAGES>;
+    using S = TcSmem<BW, BX, STAGES, XF>;
+    using CS = ClSmem<BX, STAGES, XF>;
     constexpr int MMA_N = BX;
     constexpr uint32_t TMEM_COLS = MMA_N <= 32 ? 32 : MMA_N <= 64 ? 64 : 128;
     constexpr uint32_t IDESC = umma_idesc_f16(128, MMA_N, std::is_same<T, __nv_bfloat16>::value);
-    using CS = ClSmem<BX, STAGES>;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                 ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + CS::BAR_OFF);
     uint64_t *empty = full + STAGES;
-    uint64_t *tmem_full = empty + STAGES;
+    uint64_t *xfull = empty + STAGES;
+    uint64_t *tmem_full = xfull + STAGES;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 2);
-    float *part = reinterpret_cast<float *>(smem);  // [MMA_N][128] after the ring drains
+    float *part = reinterpret_cast<float *>(smem);               // [MMA_N][128] after the ring drains
+    float *rbuf = reinterpret_cast<float *>(smem + CS::PART);    // RoPE staging [cols][128]
+    __shared__ float s_inv_rms[XF_MAX_M];
+    __shared__ float s_ssq[4][MMA_N];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -444,8 +615,9 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         prefetch_tmap(&tmW);
         prefetch_tmap(&tmX);
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], XF ? 1 + XF_WARPS : 1);
             mbar_init(&empty[s], 1);
+            mbar_init(&xfull[s], 1);
         }
         mbar_init(tmem_full, 1);
         fence_mbar_init();
@@ -456,27 +628,16 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    auto coord = [&](int i, int &kb, int &nr, int &mr) {
+        kb = kb0 + i;
+        nr = n0;
+        mr = m0;
+    };
+
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer (weights first, PDL)
-            const int pre = min(nkb, STAGES);
-            for (int i = 0; i < pre; ++i) {
-                mbar_arrive_expect_tx(&full[i], S::STAGE_BYTES);
-                tma_load_2d(smem + i * S::STAGE_BYTES, &tmW, &full[i], (kb0 + i) * TC_BK, n0, kEvictFirst);
-            }
-            pdl_wait();
-            for (int i = 0; i < pre; ++i)
-                tma_load_2d(smem + i * S::STAGE_BYTES + S::W_BYTES, &tmX, &full[i], (kb0 + i) * TC_BK,
-                            m0, kEvictLast);
-            for (int i = pre; i < nkb; ++i) {
-                const int s = i % STAGES;
-                mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
-                uint8_t *sw = smem + s * S::STAGE_BYTES;
-                mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-                tma_load_2d(sw, &tmW, &full[s], (kb0 + i) * TC_BK, n0, kEvictFirst);
-                tma_load_2d(sw + S::W_BYTES, &tmX, &full[s], (kb0 + i) * TC_BK, m0, kEvictLast);
-            }
-            pdl_trigger();
-        }
+        if (lane == 0)
+            tc_produce<S, STAGES, XF>(smem, full, empty, xfull, &tmW, &tmX, &tmU, fz.x_op == 2, nkb,
+                                      coord);
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
@@ -495,6 +656,10 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             umma_commit(tmem_full);
         }
         __syncwarp();
+    } else if (XF && warp >= 6) {
+        tc_transform<T, S, STAGES, BX>(smem, full, xfull, s_inv_rms, M, K, fz, nkb, coord, warp - 6,
+                                       lane);
+        __syncwarp();
     } else {  // ---------------- epilogue warps: TMEM -> own smem partial [col][row]
         const int quad = warp & 3;
         const int row = quad * 32 + lane;
@@ -510,13 +675,18 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     }
     tc_fence_before();
     cluster_sync_all();  // every rank's partial is in its smem
-    if (warp >= 2) {
+    if (warp >= 2 && warp <= 5) {
         pdl_wait();  // residual / C belong to earlier kernels
         const int quad = warp & 3;
         const int row = quad * 32 + lane;
         const int n = n0 + row;
+        if (fz.x_op == 3) {  // folded RMSNorm: inverse RMS of this CTA's token rows
+            inv_rms_rows(s_inv_rms, M, K, fz, threadIdx.x - 64, 128);
+            named_bar_sync(1, 128);
+        }
         const int per = (MMA_N + ck.cs - 1) / ck.cs;
         const int c_beg = (int)rank * per, c_end = min(MMA_N, c_beg + per);
+        const bool rope = fz.q_out != nullptr;
         uint32_t peer[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) peer[q] = q < ck.cs ? dsmem_map(part, q) : 0u;
@@ -529,9 +699,56 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             float o = 0.f;
 #pragma unroll
             for (int q = 0; q < 8; ++q) o += vals[q];  // rank order
-            if (n < N && m < M) {
-                if (R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
-                C[(int64_t)m * ldc + n] = Elem<T>::from_f(o);
+            const bool valid = n < N && m < M;
+            if (fz.x_op == 3 && m < M) o *= s_inv_rms[m];
+            if (valid && R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
+            const T h = Elem<T>::from_f(o);
+            const float hf = Elem<T>::to_f(h);
+            if (rope) {
+                rbuf[(c - c_beg) * 128 + row] = hf;  // rounded like the unfused qkv buffer
+            } else if (valid) {
+                C[(int64_t)m * ldc + n] = h;
+            }
+            if (fz.ssq_out) {  // per-(tile, token) sum of squares over the tile's 128 rows
+                float sq = valid ? hf * hf : 0.f;
+#pragma unroll
+                for (int o2 = 16; o2 > 0; o2 >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o2);
+                if (lane == 0) s_ssq[quad][c - c_beg] = sq;
+            }
+        }
+        if (fz.ssq_out || rope) named_bar_sync(1, 128);
+        if (fz.ssq_out && row < c_end - c_beg) {
+            const int m = m0 + c_beg + row;
+            if (m < M)
+                fz.ssq_out[(int64_t)tn * fz.ssq_out_ld + m] =
+                    s_ssq[0][row] + s_ssq[1][row] + s_ssq[2][row] + s_ssq[3][row];  // quad order
+        }
+        if (rope) {
+            // tile tn is one head: q heads [0, Hq), k heads [Hq, Hq+Hkv), v heads after
+            const int i = row & 63;
+            const float inv_freq = __powf(fz.theta, -2.f * i / 128);
+            for (int c = c_beg; c < c_end; ++c) {
+                const int m = m0 + c;
+                if (m >= M) continue;
+                const int p = fz.pos[m];
+                const float *xr = rbuf + (c - c_beg) * 128;
+                T *dst;
+                float val;
+                if (tn < fz.Hq + fz.Hkv) {
+                    float sn, cs;
+                    __sincosf(p * inv_freq, &sn, &cs);
+                    const float x0 = xr[i], x1 = xr[i + 64];
+                    val = row < 64 ? x0 * cs - x1 * sn : x1 * cs + x0 * sn;
+                    dst = tn < fz.Hq
+                              ? static_cast<T *>(fz.q_out) + ((int64_t)m * fz.Hq + tn) * 128
+                              : static_cast<T *>(fz.k_cache) + (int64_t)m * fz.cache_sb +
+                                    (int64_t)(tn - fz.Hq) * fz.cache_sh + (int64_t)p * 128;
+                } else {
+                    val = xr[row];
+                    dst = static_cast<T *>(fz.v_cache) + (int64_t)m * fz.cache_sb +
+                          (int64_t)(tn - fz.Hq - fz.Hkv) * fz.cache_sh + (int64_t)p * 128;
+                }
+                dst[row] = Elem<T>::from_f(val);
             }
         }
     }
@@ -695,11 +912,17 @@ static size_t tc_workspace(const TcPlan &pl, const fdpp_gemm_params *p) {
     return kWsCounterBytes + part;
 }
 
-template <typename T, int BX, int STAGES>
-static fdpp_status launch_cluster(const fdpp_gemm_params *p, const TcPlan &pl, const CUtensorMap &mw,
-                                  const CUtensorMap &mx, cudaStream_t st) {
-    using S = ClSmem<BX, STAGES>;
-    auto kern = gemm_cluster_kernel<T, BX, STAGES>;
+struct TcLaunch {  // everything a tcgen05 launch needs besides the plan
+    CUtensorMap mw, mx, mu;
+    GemmFuse fz;
+    bool xf;
+};
+
+template <typename T, int BX, int STAGES, bool XF>
+static fdpp_status launch_cluster(const fdpp_gemm_params *p, const TcPlan &pl, const TcLaunch &L,
+                                  cudaStream_t st) {
+    using S = ClSmem<BX, STAGES, XF>;
+    auto kern = gemm_cluster_kernel<T, BX, STAGES, XF>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -710,22 +933,22 @@ static fdpp_status launch_cluster(const fdpp_gemm_params *p, const TcPlan &pl, c
         if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_cluster)");
         attr_set = true;
     }
-    cudaError_t e = launch_kernel_cluster(kern, dim3(pl.grid, pl.wk.n_tiles_m), dim3(TC_THREADS),
-                                          S::TOTAL, st, pl.ck.cs, mw, mx, static_cast<T *>(p->c),
-                                          p->ldc, static_cast<const T *>(p->r), p->ldr, p->M, p->N,
-                                          pl.ck);
+    cudaError_t e = launch_kernel_cluster(
+        kern, dim3(pl.grid, pl.wk.n_tiles_m), dim3(XF ? TC_THREADS_XF : TC_THREADS), S::TOTAL, st,
+        pl.ck.cs, L.mw, L.mx, L.mu, static_cast<T *>(p->c), p->ldc, static_cast<const T *>(p->r),
+        p->ldr, p->M, p->N, p->K, pl.ck, L.fz);
     if (e != cudaSuccess) return cuda_status(e, "gemm_cluster_kernel launch");
     return FDPP_OK;
 }
 
-template <typename T, int BW, int BX, bool SWAP, int STAGES>
-static fdpp_status launch_tc(const fdpp_gemm_params *p, const TcPlan &pl, const CUtensorMap &mw,
-                             const CUtensorMap &mx, cudaStream_t st) {
+template <typename T, int BW, int BX, bool SWAP, int STAGES, bool XF>
+static fdpp_status launch_tc(const fdpp_gemm_params *p, const TcPlan &pl, const TcLaunch &L,
+                             cudaStream_t st) {
     if constexpr (SWAP && BW == 128) {
-        if (pl.cluster) return launch_cluster<T, BX, STAGES>(p, pl, mw, mx, st);
+        if (pl.cluster) return launch_cluster<T, BX, STAGES, XF>(p, pl, L, st);
     }
-    using S = TcSmem<BW, BX, STAGES>;
-    auto kern = gemm_tc_kernel<T, BW, BX, SWAP, STAGES>;
+    using S = TcSmem<BW, BX, STAGES, XF>;
+    auto kern = gemm_tc_kernel<T, BW, BX, SWAP, STAGES, XF>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -742,17 +965,18 @@ static fdpp_status launch_tc(const fdpp_gemm_params *p, const TcPlan &pl, const 
         counters = static_cast<int *>(p->workspace);
         ws = reinterpret_cast<float *>(static_cast<char *>(p->workspace) + kWsCounterBytes);
     }
-    cudaError_t e = launch_kernel(kern, dim3(pl.grid), dim3(TC_THREADS), S::TOTAL, st, mw, mx,
-                                  static_cast<T *>(p->c), p->ldc, static_cast<const T *>(p->r),
-                                  p->ldr, p->M, p->N, pl.wk, ws, counters);
+    cudaError_t e = launch_kernel(kern, dim3(pl.grid), dim3(XF ? TC_THREADS_XF : TC_THREADS),
+                                  S::TOTAL, st, L.mw, L.mx, L.mu, static_cast<T *>(p->c), p->ldc,
+                                  static_cast<const T *>(p->r), p->ldr, p->M, p->N, p->K, pl.wk, ws,
+                                  counters, L.fz);
     if (e != cudaSuccess) return cuda_status(e, "gemm_tc_kernel launch");
     return FDPP_OK;
 }
 
 // stage counts: 1 (single buffer), 2 (double buffer) and the deep default
 template <typename T, int BX, bool SWAP>
-static fdpp_status dispatch_stages(const fdpp_gemm_params *p, const TcPlan &pl,
-                                   const CUtensorMap &mw, const CUtensorMap &mx, cudaStream_t st) {
+static fdpp_status dispatch_stages(const fdpp_gemm_params *p, const TcPlan &pl, const TcLaunch &L,
+                                   cudaStream_t st) {
     constexpr int BW = 128;
     // default ring: ~100 KB of stages (>= 4x the ~20 KB/SM Little's-law need
     // at 6.5 TB/s), small enough that the next kernel's CTA fits beside it on
@@ -760,49 +984,103 @@ static fdpp_status dispatch_stages(const fdpp_gemm_params *p, const TcPlan &pl,
     constexpr int DEEP = (100 * 1024) / ((BW + BX) * TC_BK * 2) < 4
                              ? 4
                              : (100 * 1024) / ((BW + BX) * TC_BK * 2);
+    constexpr int DEEP_XF = (100 * 1024) / ((BW + 2 * BX) * TC_BK * 2) < 4
+                                ? 4
+                                : (100 * 1024) / ((BW + 2 * BX) * TC_BK * 2);
+    if (L.xf) {
+        if constexpr (SWAP) return launch_tc<T, BW, BX, SWAP, DEEP_XF, true>(p, pl, L, st);
+        set_error("fused activation transforms need ImplB");
+        return FDPP_ERR_UNSUPPORTED;
+    }
     switch (pl.stages) {
-        case 1: return launch_tc<T, BW, BX, SWAP, 1>(p, pl, mw, mx, st);
-        case 2: return launch_tc<T, BW, BX, SWAP, 2>(p, pl, mw, mx, st);
-        case 4: return launch_tc<T, BW, BX, SWAP, 4>(p, pl, mw, mx, st);
-        default: return launch_tc<T, BW, BX, SWAP, DEEP>(p, pl, mw, mx, st);
+        case 1: return launch_tc<T, BW, BX, SWAP, 1, false>(p, pl, L, st);
+        case 2: return launch_tc<T, BW, BX, SWAP, 2, false>(p, pl, L, st);
+        case 4: return launch_tc<T, BW, BX, SWAP, 4, false>(p, pl, L, st);
+        default: return launch_tc<T, BW, BX, SWAP, DEEP, false>(p, pl, L, st);
     }
 }
 
-static fdpp_status check_gemm(const fdpp_gemm_params *p) {
-    FDPP_REQUIRE(p && p->a && p->w && p->c, FDPP_ERR_VALUE, "null GEMM operand");
+static fdpp_status check_gemm(const fdpp_gemm_params *p, bool allow_null_c = false) {
+    FDPP_REQUIRE(p && p->a && p->w && (p->c || allow_null_c), FDPP_ERR_VALUE, "null GEMM operand");
     FDPP_REQUIRE(p->M >= 1 && p->N >= 1 && p->K >= 1, FDPP_ERR_SHAPE,
                  "GEMM dims must be >= 1, got (%d, %d, %d)", p->M, p->N, p->K);
     FDPP_REQUIRE(p->dtype == FDPP_F16 || p->dtype == FDPP_BF16, FDPP_ERR_UNSUPPORTED,
                  "GEMM dtype must be f16 or bf16");
     FDPP_REQUIRE(p->K % 8 == 0 && p->lda % 8 == 0 && p->ldw % 8 == 0 && p->ldw >= p->K &&
-                     p->lda >= p->K && p->ldc >= p->N,
+                     p->lda >= p->K && (p->c == nullptr || p->ldc >= p->N),
                  FDPP_ERR_UNSUPPORTED, "K, lda, ldw must be multiples of 8 (pad K with zeros)");
     return FDPP_OK;
 }
 
-static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st) {
-    fdpp_status s = check_gemm(p);
+static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st,
+                          const fdpp_gemm_fuse *fuse = nullptr) {
+    const bool epi_fuse = fuse && (fuse->ssq_out || fuse->q_out);
+    fdpp_status s = check_gemm(p, fuse && fuse->q_out);
     if (s != FDPP_OK) return s;
     TcPlan pl;
-    if ((s = plan_tc(p, swap, &pl)) != FDPP_OK) return s;
+    fdpp_gemm_params q = *p;
+    if (epi_fuse && q.ctas >= 0) {  // fused epilogues live in the cluster split-K kernel
+        q.ctas = 0;
+        TcPlan probe;
+        if ((s = plan_tc(&q, swap, &probe)) != FDPP_OK) return s;
+        if (!probe.cluster) q.ctas = -2;
+    }
+    if ((s = plan_tc(&q, swap, &pl)) != FDPP_OK) return s;
+    FDPP_REQUIRE(!epi_fuse || pl.cluster, FDPP_ERR_UNSUPPORTED, "fused epilogue needs cluster mode");
     FDPP_REQUIRE(tc_workspace(pl, p) <= p->workspace_bytes, FDPP_ERR_WORKSPACE,
                  "GEMM workspace too small: need %zu bytes", tc_workspace(pl, p));
-    CUtensorMap mw, mx;
-    if ((s = make_kmajor_map(&mw, p->w, p->N, p->K, p->ldw, pl.bw, p->dtype)) != FDPP_OK) return s;
-    if ((s = make_kmajor_map(&mx, p->a, p->M, p->K, p->lda, pl.bx, p->dtype)) != FDPP_OK) return s;
+    TcLaunch L;
+    memset(&L.fz, 0, sizeof(L.fz));
+    L.xf = fuse && (fuse->x_op == 1 || fuse->x_op == 2);
+    if (fuse) {
+        FDPP_REQUIRE(fuse->x_op >= 0 && fuse->x_op <= 3, FDPP_ERR_VALUE, "bad x_op %d", fuse->x_op);
+        FDPP_REQUIRE(fuse->x_op != 1 || (fuse->ssq_in && fuse->norm_w && p->M <= XF_MAX_M),
+                     FDPP_ERR_VALUE, "RMSNorm prologue needs ssq_in, norm_w and M <= %d", XF_MAX_M);
+        FDPP_REQUIRE(fuse->x_op != 3 || (fuse->ssq_in && p->M <= XF_MAX_M), FDPP_ERR_VALUE,
+                     "folded RMSNorm needs ssq_in and M <= %d", XF_MAX_M);
+        FDPP_REQUIRE(!fuse->q_out || (fuse->k_cache && fuse->v_cache && fuse->pos &&
+                                      fuse->Hq + 2 * fuse->Hkv == ceil_div(p->N, 128) &&
+                                      p->N % 128 == 0),
+                     FDPP_ERR_VALUE, "RoPE epilogue needs N = (Hq + 2 Hkv) * 128 and the caches");
+        L.fz.x_op = fuse->x_op;
+        L.fz.ssq_in = fuse->ssq_in;
+        L.fz.ssq_tiles = fuse->ssq_tiles;
+        L.fz.ssq_ld = fuse->ssq_ld;
+        L.fz.norm_w = fuse->norm_w;
+        L.fz.eps = fuse->eps;
+        L.fz.ssq_out = fuse->ssq_out;
+        L.fz.ssq_out_ld = fuse->ssq_out_ld;
+        L.fz.q_out = fuse->q_out;
+        L.fz.k_cache = fuse->k_cache;
+        L.fz.v_cache = fuse->v_cache;
+        L.fz.pos = fuse->pos;
+        L.fz.Hq = fuse->Hq;
+        L.fz.Hkv = fuse->Hkv;
+        L.fz.cache_sb = fuse->cache_stride_b;
+        L.fz.cache_sh = fuse->cache_stride_h;
+        L.fz.theta = fuse->theta;
+    }
+    if ((s = make_kmajor_map(&L.mw, p->w, p->N, p->K, p->ldw, pl.bw, p->dtype)) != FDPP_OK) return s;
+    if ((s = make_kmajor_map(&L.mx, p->a, p->M, p->K, p->lda, pl.bx, p->dtype)) != FDPP_OK) return s;
+    L.mu = L.mx;
+    if (fuse && fuse->x_op == 2) {  // silu(gate) * up: up = a[:, K:2K]
+        FDPP_REQUIRE(p->lda >= 2 * p->K, FDPP_ERR_VALUE, "SiLU prologue needs a = [gate | up]");
+        const void *up = static_cast<const char *>(p->a) + (size_t)p->K * 2;
+        if ((s = make_kmajor_map(&L.mu, up, p->M, p->K, p->lda, pl.bx, p->dtype)) != FDPP_OK) return s;
+    }
     const bool bf = p->dtype == FDPP_BF16;
     if (swap) {
         switch (pl.bx) {
-            case 16: return bf ? dispatch_stages<__nv_bfloat16, 16, true>(p, pl, mw, mx, st)
-                               : dispatch_stages<__half, 16, true>(p, pl, mw, mx, st);
-            case 32: return bf ? dispatch_stages<__nv_bfloat16, 32, true>(p, pl, mw, mx, st)
-                               : dispatch_stages<__half, 32, true>(p, pl, mw, mx, st);
-            default: return bf ? dispatch_stages<__nv_bfloat16, 64, true>(p, pl, mw, mx, st)
-                               : dispatch_stages<__half, 64, true>(p, pl, mw, mx, st);
+            case 16: return bf ? dispatch_stages<__nv_bfloat16, 16, true>(&q, pl, L, st)
+                               : dispatch_stages<__half, 16, true>(&q, pl, L, st);
+            case 32: return bf ? dispatch_stages<__nv_bfloat16, 32, true>(&q, pl, L, st)
+                               : dispatch_stages<__half, 32, true>(&q, pl, L, st);
+            default: return bf ? dispatch_stages<__nv_bfloat16, 64, true>(&q, pl, L, st)
+                               : dispatch_stages<__half, 64, true>(&q, pl, L, st);
         }
     }
-    return bf ? dispatch_stages<__nv_bfloat16, 128, false>(p, pl, mw, mx, st)
-              : dispatch_stages<__half, 128, false>(p, pl, mw, mx, st);
+    return bf ? dispatch_stages<__nv_bfloat16, 128, false>(&q, pl, L, st)
+              : dispatch_stages<__half, 128, false>(&q, pl, L, st);
 }
 
 template <typename T>
@@ -901,6 +1179,12 @@ extern "C" fdpp_status fdpp_impl_b_flat(const fdpp_gemm_params *p, void *stream)
 
 extern "C" fdpp_status fdpp_impl_c_gemm(const fdpp_gemm_params *p, void *stream) {
     return run_tc(p, false, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fdpp_status fdpp_gemm_fused(const fdpp_gemm_params *p, const fdpp_gemm_fuse *fuse,
+                                       void *stream) {
+    FDPP_REQUIRE(fuse != nullptr, FDPP_ERR_VALUE, "null fuse descriptor");
+    return run_tc(p, true, static_cast<cudaStream_t>(stream), fuse);
 }
 
 extern "C" fdpp_status fdpp_run_kernel(int32_t impl, const fdpp_gemm_params *p, void *stream) {

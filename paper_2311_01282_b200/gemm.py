@@ -161,3 +161,61 @@ def reference_call(impl: int, a, b, **kw):
         raise ShapeError("inner dims disagree")
     c = run(impl, A, pw, **kw)
     return c.float().cpu().numpy() if was_numpy else c
+
+
+def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ssq_in=None,
+              ssq_tiles: int = 0, norm_w=None, eps: float = 1e-5, ssq_out=None, rope=None,
+              stream=None, ws_tag="gemm"):
+    """ImplB with the decode-step fusions (fdpp_gemm_fused).
+
+    x_op 1: the activation tile is RMSNorm(a) * norm_w, with the rows' sums of
+    squares given as ssq_in[ssq_tiles, :] (written by the producer of ``a``).
+    x_op 2: the activation is silu(a[:, :K]) * a[:, K:] (a = fused gate|up).
+    ssq_out [N/128, M] (float32): per-128-column sums of squares of the stored
+    output rows (for the next GEMM's x_op 1).  rope = dict(q_out, k_cache,
+    v_cache, pos, theta): RoPE the q/k heads and append k/v at row pos[m]
+    (QKV projection; ``out`` unused)."""
+    torch = _torch()
+    K = pw.ldw
+    if x_op == 2:
+        if a.shape[1] < 2 * K:
+            raise ShapeError("SiLU prologue needs a = [gate | up] with 2K columns")
+    elif a.shape[1] != K:
+        raise ShapeError(f"inner dims disagree: {tuple(a.shape)} x [K={pw.K}, N={pw.N}]")
+    M = a.shape[0]
+    if out is None and rope is None:
+        out = torch.empty((M, pw.N), dtype=a.dtype, device=a.device)
+    prm = _lib.GemmParams()
+    prm.a, prm.lda = a.data_ptr(), a.stride(0)
+    prm.w, prm.ldw = pw.w.data_ptr(), pw.ldw
+    if out is not None:
+        prm.c, prm.ldc = out.data_ptr(), out.stride(0)
+    if residual is not None:
+        prm.r, prm.ldr = residual.data_ptr(), residual.stride(0)
+    prm.M, prm.N, prm.K = M, pw.N, K
+    prm.dtype = _lib.dtype_code(a.dtype)
+    fz = _lib.GemmFuse()
+    fz.x_op = int(x_op)
+    if x_op in (1, 3):
+        fz.ssq_in, fz.ssq_tiles, fz.ssq_ld = ssq_in.data_ptr(), int(ssq_tiles), ssq_in.stride(0)
+        fz.eps = float(eps)
+    if x_op == 1:
+        fz.norm_w = norm_w.data_ptr()
+    if ssq_out is not None:
+        fz.ssq_out, fz.ssq_out_ld = ssq_out.data_ptr(), ssq_out.stride(0)
+    if rope is not None:
+        kc = rope["k_cache"]
+        fz.q_out, fz.k_cache, fz.v_cache = rope["q_out"].data_ptr(), kc.data_ptr(), rope["v_cache"].data_ptr()
+        fz.pos = rope["pos"].data_ptr()
+        fz.Hq, fz.Hkv = rope["q_out"].shape[1], kc.shape[1]
+        fz.cache_stride_b, fz.cache_stride_h = kc.stride(0), kc.stride(1)
+        fz.theta = float(rope.get("theta", 10000.0))
+    lib = _lib.load()
+    need = ctypes.c_size_t()
+    _lib.check(lib.fdpp_gemm_workspace_size(IMPL_B, ctypes.byref(prm), ctypes.byref(need)), "gemm_fused")
+    if need.value:
+        ws = workspace.get(need.value, a.device, tag=ws_tag)
+        prm.workspace, prm.workspace_bytes = ws.data_ptr(), ws.numel()
+    _lib.check(lib.fdpp_gemm_fused(ctypes.byref(prm), ctypes.byref(fz), _lib.stream_handle(stream)),
+               "gemm_fused")
+    return out

@@ -30,7 +30,7 @@ import torch
 from . import _lib, workspace
 from . import dispatch as _dispatch_mod  # noqa: F401  (module, not the function)
 from .attention import AttentionConfig, decode_attention
-from .gemm import PackedWeight
+from .gemm import PackedWeight, run_fused
 from .softmax import ScalingCalibration
 
 import importlib
@@ -84,12 +84,24 @@ def build_dispatch_table(cfg: LlamaConfig, m_sweep=D.B200_M_SWEEP, reps=5, dtype
     return table
 
 
+def fold_norm(pw: PackedWeight, norm_w) -> PackedWeight:
+    """W'[n, k] = W[n, k] * w[k]: RMSNorm's weight folded into the next
+    projection, so the GEMM consumes the raw residual stream and only scales
+    each output row by its inverse RMS in the epilogue (fdpp_gemm_fuse x_op 3).
+    All-ones weights (random init) return the same tensor."""
+    if bool((norm_w == 1).all()):
+        return pw
+    w = pw.w.clone()
+    w[:, : pw.K] = (w[:, : pw.K].float() * norm_w.float()[None, :]).to(w.dtype)
+    return PackedWeight(w, pw.K, pw.N)
+
+
 class LlamaDecoder:
     """Random-init Llama decode engine over libfdpp (one replica per GPU)."""
 
     def __init__(self, cfg: LlamaConfig, batch: int, max_len: int, *, table=None,
                  calib: ScalingCalibration = GOLDEN_CALIB, dtype=torch.float16, seed: int = 0,
-                 attn_p: int = 0, attn_splits: int = 0, n_layers: int = None):
+                 attn_p: int = 0, attn_splits: int = 0, n_layers: int = None, fused: bool = True):
         _lib.require_cuda()
         self.cfg, self.B, self.max_len, self.dtype = cfg, batch, max_len, dtype
         self.n_layers = n_layers or cfg.n_layers
@@ -131,6 +143,14 @@ class LlamaDecoder:
         self.pos = torch.zeros(B, dtype=torch.int32, device=dev)
         self.lens = torch.ones(B, dtype=torch.int32, device=dev)
         self.row_flags = torch.zeros((B, Hq), dtype=torch.uint8, device=dev)
+        # fused step: per-(128-column tile, row) sums of squares of the residual
+        # stream, written by the embed / O / down epilogues, read by the next
+        # GEMM's RMSNorm prologue
+        self.fused = fused
+        nt = max(1, -(-cfg.hidden // 128))
+        self.ssq_a = torch.zeros((nt, B), dtype=torch.float32, device=dev)
+        self.ssq_b = torch.zeros((nt, B), dtype=torch.float32, device=dev)
+        self.ssq_tiles = nt
         self.recomputed = torch.zeros(1, dtype=torch.int32, device=dev)
         self.attn_cfg = AttentionConfig(p=attn_p, scale=1.0 / math.sqrt(Dh), calib=calib,
                                         splits_per_chunk=attn_splits)
@@ -138,8 +158,19 @@ class LlamaDecoder:
             table = build_dispatch_table(cfg, dtype=dtype)
         self.table = table
         self.choices = {op: D.dispatch(B, n, k, table) for op, (n, k) in shapes.items()}
+        # the fused step is built on ImplB (prologue/epilogue fusions); use it when
+        # the dispatch table picks ImplB for every projection at this batch
+        fused = fused and all(c == D.KernelChoice.IMPL_B for c in self.choices.values())
         self.graph = None
-        self.launches_per_step = 1 + self.n_layers * 10 + 4
+        if fused:  # fold the RMSNorm weights into the following projections' columns
+            for L in self.layers:
+                L["qkv_f"] = fold_norm(L["qkv"], L["ln1"])
+                L["gate_up_f"] = fold_norm(L["gate_up"], L["ln2"])
+            self.lm_head_f = fold_norm(self.lm_head, self.ln_f)
+        self.fused = fused
+        # fused: embed + L x (qkv+rope, attn async, attn recompute, o, gate_up, silu, down)
+        #        + lm_head + argmax + advance
+        self.launches_per_step = (1 + self.n_layers * 7 + 3) if fused else (1 + self.n_layers * 10 + 4)
 
     # ------------------------------------------------------------------ state
     def prefill_random(self, L: int, seed: int = 1):
@@ -160,12 +191,55 @@ class LlamaDecoder:
 
     def enqueue_step(self):
         """Enqueue one decode step on the current stream (no host sync)."""
+        if self.fused:
+            return self._enqueue_fused()
+        return self._enqueue_unfused()
+
+    def _enqueue_fused(self):
+        """Seven launches per layer.  RMSNorm is folded: its weight is
+        pre-multiplied into the QKV / gate|up / LM-head weight columns and each
+        output row is scaled by its inverse RMS in the GEMM epilogue, from the
+        per-(tile, row) sums of squares the previous residual GEMM's epilogue
+        (or the embedding) wrote.  RoPE + KV append run in the QKV epilogue, the
+        residual adds in the O / down epilogues."""
+        cfg, B, dt = self.cfg, self.B, _lib.dtype_code(self.dtype)
+        lib = _lib.load()
+        st = _lib.stream_handle()
+        Hq, Dh = cfg.n_heads, cfg.head_dim
+        _lib.check(lib.fdpp_embed(self.ids.data_ptr(), self.embed.data_ptr(), self.x.data_ptr(), B,
+                                  cfg.hidden, self.ssq_a.data_ptr(), dt, st), "embed")
+        ssq_tiles = 1
+        for li, L in enumerate(self.layers):
+            kc, vc = self.k_cache[li], self.v_cache[li]
+            run_fused(self.x, L["qkv_f"], x_op=3, ssq_in=self.ssq_a, ssq_tiles=ssq_tiles,
+                      eps=cfg.eps, ws_tag="decode_gemm",
+                      rope={"q_out": self.q, "k_cache": kc, "v_cache": vc, "pos": self.pos,
+                            "theta": cfg.rope_theta})
+            decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
+                             seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed)
+            run_fused(self.attn.view(B, Hq * Dh), L["o"], out=self.x, residual=self.x,
+                      ssq_out=self.ssq_b, ws_tag="decode_gemm")
+            run_fused(self.x, L["gate_up_f"], out=self.gu, x_op=3, ssq_in=self.ssq_b,
+                      ssq_tiles=self.ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
+            _lib.check(lib.fdpp_silu_mul(self.gu.data_ptr(), self.act.data_ptr(), B, cfg.ffn, dt, st),
+                       "silu_mul")
+            run_fused(self.act, L["down"], out=self.x, residual=self.x, ssq_out=self.ssq_a,
+                      ws_tag="decode_gemm")
+            ssq_tiles = self.ssq_tiles
+        run_fused(self.x, self.lm_head_f, out=self.logits, x_op=3, ssq_in=self.ssq_a,
+                  ssq_tiles=ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
+        _lib.check(lib.fdpp_argmax(self.logits.data_ptr(), self.ids.data_ptr(), B, cfg.vocab, dt, st),
+                   "argmax")
+        _lib.check(lib.fdpp_advance_positions(self.pos.data_ptr(), self.lens.data_ptr(), B, st),
+                   "advance")
+
+    def _enqueue_unfused(self):
         cfg, B, dt = self.cfg, self.B, _lib.dtype_code(self.dtype)
         lib = _lib.load()
         st = _lib.stream_handle()
         Hq, Hkv, Dh = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
         _lib.check(lib.fdpp_embed(self.ids.data_ptr(), self.embed.data_ptr(), self.x.data_ptr(), B,
-                                  cfg.hidden, dt, st), "embed")
+                                  cfg.hidden, None, dt, st), "embed")
         for li, L in enumerate(self.layers):
             _lib.check(lib.fdpp_rmsnorm(self.x.data_ptr(), L["ln1"].data_ptr(), self.h.data_ptr(), B,
                                         cfg.hidden, cfg.eps, dt, st), "rmsnorm")

@@ -1,0 +1,140 @@
+"""The decode step (caller of the hot path): the fused GEMM
+prologues/epilogues against the standalone glue kernels, the fused step
+against the unfused step, and graph replay against eager execution."""
+
+import importlib
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+@pytest.fixture(scope="module")
+def mods():
+    import paper_2311_01282_b200 as fd
+    from paper_2311_01282_b200 import _lib, gemm, llama
+    D = importlib.import_module("paper_2311_01282_b200.dispatch")
+    return fd, _lib, gemm, llama, D
+
+
+def _rel(a, b):
+    a = a.float().cpu().numpy().reshape(a.shape[0], -1)
+    b = b.float().cpu().numpy().reshape(b.shape[0], -1)
+    return float((np.abs(a - b).max(axis=1) / np.maximum(np.abs(b).max(axis=1), 1e-8)).max())
+
+
+def test_fused_rmsnorm_prologue_and_ssq_epilogue(torch, mods):
+    fd, _lib, gemm, _, D = mods
+    B, H, N = 8, 4096, 12288
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn((B, H), generator=g, device="cuda").half()
+    w_ln = (1 + 0.1 * torch.randn(H, generator=g, device="cuda")).half()
+    pw = gemm.PackedWeight((torch.randn((N, H), generator=g, device="cuda") / 64).half(), H, N)
+    # producer side: a residual GEMM whose epilogue emits the row sums of squares
+    po = gemm.PackedWeight((torch.randn((H, H), generator=g, device="cuda") / 64).half(), H, H)
+    a0 = torch.randn((B, H), generator=g, device="cuda").half()
+    ssq = torch.zeros((H // 128, B), dtype=torch.float32, device="cuda")
+    xr = x.clone()
+    gemm.run_fused(a0, po, out=xr, residual=xr, ssq_out=ssq)
+    ref_x = D.run_device(D.KernelChoice.IMPL_B, a0, po, residual=x)
+    assert torch.equal(xr, ref_x)                       # same reduction path, bitwise
+    assert torch.allclose(ssq.sum(0), xr.float().pow(2).sum(1), rtol=1e-5, atol=1e-3)
+    # consumer side: RMSNorm fused into the activation tile
+    out = gemm.run_fused(xr, pw, x_op=1, ssq_in=ssq, ssq_tiles=H // 128, norm_w=w_ln, eps=1e-5)
+    h = torch.empty_like(xr)
+    lib = _lib.load()
+    _lib.check(lib.fdpp_rmsnorm(xr.data_ptr(), w_ln.data_ptr(), h.data_ptr(), B, H, 1e-5, 0,
+                                _lib.stream_handle()))
+    ref = D.run_device(D.KernelChoice.IMPL_B, h, pw)
+    assert _rel(out, ref) <= 2e-3
+
+
+def test_folded_rmsnorm_epilogue(torch, mods):
+    fd, _lib, gemm, llama, D = mods
+    B, H, N = 8, 4096, 22016
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn((B, H), generator=g, device="cuda").half()
+    w_ln = (1 + 0.1 * torch.randn(H, generator=g, device="cuda")).half()
+    pw = gemm.PackedWeight((torch.randn((N, H), generator=g, device="cuda") / 64).half(), H, N)
+    ssq = x.float().pow(2).sum(1)[None, :].contiguous()            # one "tile"
+    out = gemm.run_fused(x, llama.fold_norm(pw, w_ln), x_op=3, ssq_in=ssq, ssq_tiles=1, eps=1e-5)
+    h = torch.empty_like(x)
+    lib = _lib.load()
+    _lib.check(lib.fdpp_rmsnorm(x.data_ptr(), w_ln.data_ptr(), h.data_ptr(), B, H, 1e-5, 0,
+                                _lib.stream_handle()))
+    ref = D.run_device(D.KernelChoice.IMPL_B, h, pw)
+    assert _rel(out, ref) <= 3e-3
+
+
+def test_fused_silu_prologue(torch, mods):
+    fd, _lib, gemm, _, D = mods
+    B, F, H = 16, 11008, 4096
+    g = torch.Generator(device="cuda").manual_seed(1)
+    gu = torch.randn((B, 2 * F), generator=g, device="cuda").half()
+    pw = gemm.PackedWeight((torch.randn((H, F), generator=g, device="cuda") / 100).half(), F, H)
+    res = torch.randn((B, H), generator=g, device="cuda").half()
+    out = res.clone()
+    gemm.run_fused(gu, pw, out=out, residual=out, x_op=2)
+    act = torch.empty((B, F), dtype=torch.half, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.fdpp_silu_mul(gu.data_ptr(), act.data_ptr(), B, F, 0, _lib.stream_handle()))
+    ref = D.run_device(D.KernelChoice.IMPL_B, act, pw, residual=res)
+    assert torch.equal(out, ref)        # identical activation bits, identical GEMM path
+
+
+def test_fused_rope_append_epilogue(torch, mods):
+    fd, _lib, gemm, _, D = mods
+    B, H, Hq, Hkv, Dh, Lmax = 4, 4096, 32, 32, 128, 40
+    g = torch.Generator(device="cuda").manual_seed(2)
+    h = torch.randn((B, H), generator=g, device="cuda").half()
+    N = (Hq + 2 * Hkv) * Dh
+    pw = gemm.PackedWeight((torch.randn((N, H), generator=g, device="cuda") / 64).half(), H, N)
+    pos = torch.tensor([3, 17, 0, 39], dtype=torch.int32, device="cuda")
+    kc = torch.zeros((B, Hkv, Lmax, Dh), dtype=torch.half, device="cuda")
+    vc = torch.zeros_like(kc)
+    q = torch.zeros((B, Hq, Dh), dtype=torch.half, device="cuda")
+    gemm.run_fused(h, pw, rope={"q_out": q, "k_cache": kc, "v_cache": vc, "pos": pos, "theta": 10000.0})
+    qkv = D.run_device(D.KernelChoice.IMPL_B, h, pw, ctas=-2)     # same cluster split
+    kc2, vc2, q2 = torch.zeros_like(kc), torch.zeros_like(vc), torch.zeros_like(q)
+    lib = _lib.load()
+    _lib.check(lib.fdpp_rope_append(qkv.data_ptr(), q2.data_ptr(), kc2.data_ptr(), vc2.data_ptr(),
+                                    pos.data_ptr(), B, Hq, Hkv, Dh, kc2.stride(0), kc2.stride(1),
+                                    10000.0, 0, _lib.stream_handle()))
+    assert torch.equal(q, q2) and torch.equal(kc, kc2) and torch.equal(vc, vc2)
+
+
+def _decoder(torch, mods, fused, layers=2, B=4, L=64):
+    fd, _lib, gemm, llama, D = mods
+    table = D.DispatchTable(fingerprint="test")
+    for n, k in llama.LLAMA2_7B.gemm_shapes().values():
+        table.add(D.DispatchEntry(n=n, k=k, m1=1, m2=128))
+    dec = llama.LlamaDecoder(llama.LLAMA2_7B, B, L + 8, table=table, seed=5, n_layers=layers,
+                             fused=fused)
+    dec.prefill_random(L, seed=6)
+    return dec
+
+
+def test_fused_step_matches_unfused_step(torch, mods):
+    a = _decoder(torch, mods, fused=True)
+    b = _decoder(torch, mods, fused=False)
+    a.enqueue_step()
+    b.enqueue_step()
+    torch.cuda.synchronize()
+    assert _rel(a.logits, b.logits) <= 2e-2
+    for li in range(a.n_layers):
+        assert _rel(a.k_cache[li][:, :, 64], b.k_cache[li][:, :, 64]) <= 2e-2
+    # graph replay == eager for the next step
+    a.capture()
+    s0 = a.pos.clone()
+    a.step()
+    torch.cuda.synchronize()
+    assert torch.equal(a.pos, s0 + 1)
