@@ -161,6 +161,7 @@ struct GemmFuse {
     int Hq, Hkv;
     int64_t cache_sb, cache_sh;
     float theta;
+    int l2pf;                       // weight k-blocks prefetched to L2 ahead of the ring
 };
 
 template <int BW, int BX, int STAGES, bool XF = false>
@@ -183,6 +184,15 @@ template <typename T, int BW, bool SWAP>
 __device__ __forceinline__ void epi_store16(const float (&v)[16], T *C, int64_t ldc, const T *R,
                                             int64_t ldr, int M, int N, int n0, int m0, int row,
                                             int c0, const float *row_scale) {
+    // all residual loads first (one round trip), then the stores; R may alias
+    // C, but every (m, n) is read and written by this thread only
+    float r[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        const int n = SWAP ? n0 + row : n0 + c0 + j;
+        const int m = SWAP ? m0 + c0 + j : m0 + row;
+        r[j] = (R && n < N && m < M) ? Elem<T>::to_f(R[(int64_t)m * ldr + n]) : 0.f;
+    }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         const int n = SWAP ? n0 + row : n0 + c0 + j;
@@ -190,8 +200,7 @@ __device__ __forceinline__ void epi_store16(const float (&v)[16], T *C, int64_t 
         if (n < N && m < M) {
             float o = v[j];
             if (row_scale) o *= row_scale[m];  // folded RMSNorm: inverse RMS of token m
-            if (R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
-            C[(int64_t)m * ldc + n] = Elem<T>::from_f(o);
+            C[(int64_t)m * ldc + n] = Elem<T>::from_f(o + r[j]);
         }
     }
 }
@@ -222,7 +231,7 @@ template <typename S, int STAGES, bool XF, typename Coord>
 __device__ __forceinline__ void tc_produce(uint8_t *smem, uint64_t *full, uint64_t *empty,
                                            uint64_t *xfull, const CUtensorMap *tmW,
                                            const CUtensorMap *tmX, const CUtensorMap *tmU,
-                                           bool with_up, int n, Coord coord) {
+                                           bool with_up, int n, int l2pf, Coord coord) {
     constexpr uint32_t WB = S::W_BYTES, XB = S::X_BYTES;
     const uint32_t xbytes = XB * (with_up ? 2 : 1);
     auto load_x = [&](int i, int s) {
@@ -242,6 +251,13 @@ __device__ __forceinline__ void tc_produce(uint8_t *smem, uint64_t *full, uint64
         coord(i, kb, nr, mr);
         mbar_arrive_expect_tx(&full[i], XF ? WB : WB + XB);
         tma_load_2d(smem + i * S::STAGE_BYTES, tmW, &full[i], kb * TC_BK, nr, kEvictFirst);
+    }
+    // ... and pull the next k-blocks toward L2 so the HBM stays busy across the
+    // predecessor's tail (this CTA may be resident long before pdl_wait returns)
+    for (int i = pre; i < min(n, pre + l2pf); ++i) {
+        int kb, nr, mr;
+        coord(i, kb, nr, mr);
+        tma_prefetch_2d(tmW, kb * TC_BK, nr);
     }
     pdl_wait();
     for (int i = 0; i < pre; ++i) load_x(i, i);
@@ -419,7 +435,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
     if (warp == 0) {
         if (lane == 0)
             tc_produce<S, STAGES, XF>(smem, full, empty, xfull, &tmW, &tmX, &tmU, fz.x_op == 2,
-                                      u1 - u0, coord);
+                                      u1 - u0, fz.l2pf, coord);
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
             int seg = 0;
@@ -573,13 +589,123 @@ template <int BX, int STAGES, bool XF>
 struct ClSmem {
     using S = TcSmem<128, BX, STAGES, XF>;
     static constexpr uint32_t RING = STAGES * S::STAGE_BYTES;
-    static constexpr uint32_t PART = BX * 128 * 4;  // fp32 partial [MMA_N][128]
+    // fp32 partial in 4-column groups, [BX/4][128 rows][4]: a warp's 16-B
+    // accesses of one group cover 512 contiguous bytes (local and DSMEM)
+    static constexpr uint32_t PART = BX * 128 * 4;
     static constexpr uint32_t BAR_OFF = RING > 2 * PART ? RING : 2 * PART;  // + RoPE staging
     static constexpr uint32_t TOTAL = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;
 };
 
+// Epilogue of the cluster split-K kernel for one thread (= one weight row n):
+// sum the CS ranks' fp32 partials of columns [c_beg, c_end) in rank order,
+// apply the folded-RMSNorm row scale and the residual, write C (or stage for
+// RoPE) and the per-column sums of squares.  Every DSMEM and residual load of
+// the slice is issued before the first add (one round trip, not one per column).
+template <typename T>
+struct ClEpi {
+    const float *part;
+    float *rbuf;
+    T *C;
+    int64_t ldc;
+    const T *R;
+    int64_t ldr;
+    int M, N, n0, m0, c_beg, c_end, row, lane, quad;
+    bool rope;
+    const float *inv_rms;  // folded RMSNorm (nullptr: none)
+    float *ssq;            // s_ssq[4][MMA_N] (nullptr: none)
+};
+
+template <typename T, int MMA_N>
+__device__ __forceinline__ void cl_store_col(const ClEpi<T> &e, int c, float o, float r) {
+    const int m = e.m0 + c, n = e.n0 + e.row;
+    const bool valid = n < e.N && m < e.M;
+    if (e.inv_rms && m < e.M) o *= e.inv_rms[m];
+    const T h = Elem<T>::from_f(o + r);
+    const float hf = Elem<T>::to_f(h);
+    if (e.rope) {
+        e.rbuf[(c - e.c_beg) * 128 + e.row] = hf;  // rounded like the unfused qkv buffer
+    } else if (valid) {
+        e.C[(int64_t)m * e.ldc + n] = h;
+    }
+    if (e.ssq) {  // per-(tile, token) sum of squares over the tile's 128 rows
+        float sq = valid ? hf * hf : 0.f;
+#pragma unroll
+        for (int o2 = 16; o2 > 0; o2 >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o2);
+        if (e.lane == 0) e.ssq[e.quad * MMA_N + (c - e.c_beg)] = sq;
+    }
+}
+
+template <typename T, int MMA_N, int CS>
+__device__ __forceinline__ void cl_reduce_store(const ClEpi<T> &e) {
+    constexpr int PER = (((MMA_N + CS - 1) / CS) + 3) & ~3;
+    constexpr int NG = PER / 4;
+    const int n = e.n0 + e.row;
+    const uint32_t base = smem_u32(e.part) + (uint32_t)(((e.c_beg >> 2) * 128 + e.row) * 16);
+    float4 buf[NG][CS];
+    float rv[PER];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        const bool live = e.c_beg + 4 * g < e.c_end && e.m0 + e.c_beg + 4 * g < e.M;
+#pragma unroll
+        for (int q = 0; q < CS; ++q)
+            buf[g][q] = live ? dsmem_ld_v4(dsmem_map_addr(base + 2048u * g, q))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int m = e.m0 + e.c_beg + j;
+        rv[j] = (e.R && e.c_beg + j < e.c_end && m < e.M && n < e.N)
+                    ? Elem<T>::to_f(e.R[(int64_t)m * e.ldr + n])
+                    : 0.f;
+    }
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        if (e.c_beg + 4 * g >= e.c_end) break;
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < CS; ++q) {  // rank order
+            o[0] += buf[g][q].x;
+            o[1] += buf[g][q].y;
+            o[2] += buf[g][q].z;
+            o[3] += buf[g][q].w;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cl_store_col<T, MMA_N>(e, e.c_beg + 4 * g + j, o[j], rv[4 * g + j]);
+    }
+}
+
+// any cluster size (rank count not a power of two): one 4-column group at a time
+template <typename T, int MMA_N>
+__device__ __forceinline__ void cl_reduce_store_any(const ClEpi<T> &e, int cs) {
+    const int n = e.n0 + e.row;
+    const uint32_t base = smem_u32(e.part) + (uint32_t)(((e.c_beg >> 2) * 128 + e.row) * 16);
+    for (int c = e.c_beg; c < e.c_end; c += 4) {
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int q0 = 0; q0 < cs; q0 += 8) {  // up to 8 loads in flight, rank order
+            float4 v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                v[q] = q0 + q < cs ? dsmem_ld_v4(dsmem_map_addr(base + 512u * (c - e.c_beg), q0 + q))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                o[0] += v[q].x;
+                o[1] += v[q].y;
+                o[2] += v[q].z;
+                o[3] += v[q].w;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int m = e.m0 + c + j;
+            const float r = (e.R && m < e.M && n < e.N) ? Elem<T>::to_f(e.R[(int64_t)m * e.ldr + n]) : 0.f;
+            cl_store_col<T, MMA_N>(e, c + j, o[j], r);
+        }
+    }
+}
+
 template <typename T, int BX, int STAGES, bool XF>
-__global__ void __launch_bounds__(XF ? TC_THREADS_XF : TC_THREADS, XF ? 2 : 1)
+__global__ void __launch_bounds__(XF ? TC_THREADS_XF : TC_THREADS, 2)  // 2 CTAs / SM
 gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                     const __grid_constant__ CUtensorMap tmU, T *C, int64_t ldc,
                     const T *R /* may alias C */, int64_t ldr, int M, int N, int K,
@@ -599,7 +725,7 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     uint64_t *xfull = empty + STAGES;
     uint64_t *tmem_full = xfull + STAGES;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 2);
-    float *part = reinterpret_cast<float *>(smem);               // [MMA_N][128] after the ring drains
+    float *part = reinterpret_cast<float *>(smem);               // [BX/4][128][4] after the ring drains
     float *rbuf = reinterpret_cast<float *>(smem + CS::PART);    // RoPE staging [cols][128]
     __shared__ float s_inv_rms[XF_MAX_M];
     __shared__ float s_ssq[4][MMA_N];
@@ -637,7 +763,7 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     if (warp == 0) {
         if (lane == 0)
             tc_produce<S, STAGES, XF>(smem, full, empty, xfull, &tmW, &tmX, &tmU, fz.x_op == 2, nkb,
-                                      coord);
+                                      fz.l2pf, coord);
         __syncwarp();
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
@@ -670,7 +796,9 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             float v[16];
             tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + c0, v);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) part[(c0 + j) * 128 + row] = v[j];
+            for (int j = 0; j < 16; j += 4)
+                *reinterpret_cast<float4 *>(part + (((c0 + j) >> 2) * 128 + row) * 4) =
+                    make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
     }
     tc_fence_before();
@@ -684,37 +812,17 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             inv_rms_rows(s_inv_rms, M, K, fz, threadIdx.x - 64, 128);
             named_bar_sync(1, 128);
         }
-        const int per = (MMA_N + ck.cs - 1) / ck.cs;
+        // column slice of this rank: a multiple of 4 columns (16-B DSMEM loads)
+        const int per = (((MMA_N + ck.cs - 1) / ck.cs) + 3) & ~3;
         const int c_beg = (int)rank * per, c_end = min(MMA_N, c_beg + per);
         const bool rope = fz.q_out != nullptr;
-        uint32_t peer[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) peer[q] = q < ck.cs ? dsmem_map(part, q) : 0u;
-        for (int c = c_beg; c < c_end; ++c) {
-            const int m = m0 + c;
-            float vals[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                vals[q] = q < ck.cs ? dsmem_ld_f32(peer[q] + (uint32_t)((c * 128 + row) * 4)) : 0.f;
-            float o = 0.f;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) o += vals[q];  // rank order
-            const bool valid = n < N && m < M;
-            if (fz.x_op == 3 && m < M) o *= s_inv_rms[m];
-            if (valid && R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
-            const T h = Elem<T>::from_f(o);
-            const float hf = Elem<T>::to_f(h);
-            if (rope) {
-                rbuf[(c - c_beg) * 128 + row] = hf;  // rounded like the unfused qkv buffer
-            } else if (valid) {
-                C[(int64_t)m * ldc + n] = h;
-            }
-            if (fz.ssq_out) {  // per-(tile, token) sum of squares over the tile's 128 rows
-                float sq = valid ? hf * hf : 0.f;
-#pragma unroll
-                for (int o2 = 16; o2 > 0; o2 >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o2);
-                if (lane == 0) s_ssq[quad][c - c_beg] = sq;
-            }
+        ClEpi<T> ep{part, rbuf, C, ldc, R, ldr, M, N, n0, m0, c_beg, c_end, row, lane, quad, rope,
+                    fz.x_op == 3 ? s_inv_rms : nullptr, fz.ssq_out ? &s_ssq[0][0] : nullptr};
+        switch (ck.cs) {
+            case 2: cl_reduce_store<T, MMA_N, 2>(ep); break;
+            case 4: cl_reduce_store<T, MMA_N, 4>(ep); break;
+            case 8: cl_reduce_store<T, MMA_N, 8>(ep); break;
+            default: cl_reduce_store_any<T, MMA_N>(ep, ck.cs); break;
         }
         if (fz.ssq_out || rope) named_bar_sync(1, 128);
         if (fz.ssq_out && row < c_end - c_beg) {
@@ -870,13 +978,15 @@ static fdpp_status plan_tc(const fdpp_gemm_params *p, bool swap, TcPlan *pl) {
     const int sms = sm_count() > 0 ? sm_count() : 148;
     const int tiles = w.n_tiles_n * w.n_tiles_m;
     // Auto policy for ImplB (measured in-graph on B200 across the Llama shapes,
-    // tools/mode_sweep.py): few tiles -> cluster split-K, 8 CTAs per tile for
-    // <= 40 tiles (e.g. N = 4096), 2 per tile up to ~0.9 SMs of tiles (N = 12288);
-    // many tiles -> stream-K with two CTAs per SM.  ctas < 0 forces cs = -ctas.
-    pl->cluster = swap && ((p->ctas == 0 && tiles <= (sms * 9) / 10) || p->ctas < 0);
+    // tools/cs_sweep.py, profiles/r1_gemm_modes.txt): cluster split-K with 8
+    // CTAs per tile for <= 40 tiles (e.g. N = 4096), 2 per tile up to ~0.9 SMs
+    // of tiles (N = 12288), one CTA per tile while every tile fits in one wave
+    // at two CTAs per SM (N = 22016, 32000); beyond that, stream-K with two
+    // CTAs per SM.  ctas < 0 forces cs = -ctas.
+    pl->cluster = swap && ((p->ctas == 0 && tiles <= 2 * sms) || p->ctas < 0);
     if (pl->cluster) {
-        int cs = p->ctas < 0 ? -p->ctas : (tiles <= 40 ? 8 : 2);
-        cs = cs < 1 ? 1 : (cs > 8 ? 8 : cs);
+        int cs = p->ctas < 0 ? -p->ctas : (tiles <= 40 ? 8 : tiles <= (sms * 9) / 10 ? 2 : 1);
+        cs = cs < 1 ? 1 : (cs > 16 ? 16 : cs);  // > 8: non-portable cluster size
         if (cs > kb_total) cs = kb_total;
         TcCluster &c = pl->ck;
         c.n_tiles_n = w.n_tiles_n;
@@ -930,6 +1040,8 @@ static fdpp_status launch_cluster(const fdpp_gemm_params *p, const TcPlan &pl, c
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_cluster)");
         attr_set = true;
     }
@@ -1012,6 +1124,16 @@ static fdpp_status check_gemm(const fdpp_gemm_params *p, bool allow_null_c = fal
     return FDPP_OK;
 }
 
+// Weight k-blocks each CTA prefetches to L2 before waiting on its predecessor
+// (FDPP_L2PF overrides; 0 disables).
+static int l2_prefetch_blocks() {
+    static int v = [] {
+        const char *e = getenv("FDPP_L2PF");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st,
                           const fdpp_gemm_fuse *fuse = nullptr) {
     const bool epi_fuse = fuse && (fuse->ssq_out || fuse->q_out);
@@ -1031,6 +1153,7 @@ static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st,
                  "GEMM workspace too small: need %zu bytes", tc_workspace(pl, p));
     TcLaunch L;
     memset(&L.fz, 0, sizeof(L.fz));
+    L.fz.l2pf = l2_prefetch_blocks();
     L.xf = fuse && (fuse->x_op == 1 || fuse->x_op == 2);
     if (fuse) {
         FDPP_REQUIRE(fuse->x_op >= 0 && fuse->x_op <= 3, FDPP_ERR_VALUE, "bad x_op %d", fuse->x_op);
