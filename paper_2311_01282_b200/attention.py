@@ -129,9 +129,10 @@ def _torch():
     return torch
 
 
-def plan(q, k_cache, cfg: AttentionConfig, L: Optional[int] = None):
-    """(p, splits_per_chunk) the library will use for these shapes."""
-    prm = _params(q, k_cache, k_cache, q, cfg, "sync", L)
+def plan(q, k_cache, cfg: AttentionConfig, L: Optional[int] = None, mode: str = "async"):
+    """(p, splits_per_chunk) the library will use for these shapes in `mode`
+    (the async launch may run the persistent kernel, whose auto p is 1)."""
+    prm = _params(q, k_cache, k_cache, q, cfg, mode, L)
     c, s = ctypes.c_int32(), ctypes.c_int32()
     _lib.check(_lib.load().fdpp_attn_plan(ctypes.byref(prm), ctypes.byref(c), ctypes.byref(s)), "attn_plan")
     return c.value, s.value
