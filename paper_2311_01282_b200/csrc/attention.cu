@@ -20,6 +20,8 @@
 //   flagged row exit before touching memory, so the launch can always be made
 //   (graph-capturable, no host round trip).
 #include <cfloat>
+#include <cmath>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -37,6 +39,8 @@ struct AttnArgs {
     int64_t q_sb, q_sh, kv_sb, kv_sh, o_sb, o_sh;
     const int32_t *seq_lens;
     float scale, phi, a, b;
+    float pscale, inv_pscale;  // MMA path: power-of-two scale keeping e^(x-phi) in fp16 range
+    int64_t kv_rows_per_head;  // MMA path: rows of one (batch, kv-head) in the 2-D K/V maps
     int p, nsub;
     uint8_t *row_flags;
     int32_t *viol_index;
@@ -90,16 +94,68 @@ __device__ __forceinline__ float safe_scale(float m, float mref) {
     return m == -INFINITY ? 0.f : __expf(m - mref);
 }
 
-template <typename T, int D, int GT, bool ASYNC>
-__global__ void __launch_bounds__(ATT_THREADS)
-attn_split_kernel(const AttnArgs args) {
+// ---- tensor-core (mma.sync) helpers for the GQA/MQA consumer
+template <typename T>
+__device__ __forceinline__ void mma_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value)
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+    else
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+        return *reinterpret_cast<uint32_t *>(&v);
+    } else {
+        __half2 v = __floats2half2_rn(lo, hi);
+        return *reinterpret_cast<uint32_t *>(&v);
+    }
+}
+
+// MMA = true: the GQA/MQA async path on tensor cores (mma.sync.m16n8k16; a
+// decode step needs ~16 flop/B x HBM bandwidth ~ 0.1-0.2 PFLOP/s, the legacy
+// pipe sustains ~0.55 PFLOP/s on B200: profiles/r1_mma_sync_throughput.txt).
+// GT = 16 query rows of one kv head on the MMA M axis; K/V tiles arrive by
+// 2-D TMA in the 128-byte swizzle (ldmatrix reads them conflict-free); per
+// 16-key slice S = Q K^T, the unified-phi band check and e^(x - phi) in fp32
+// (exp-sums stay fp32), P = e * pscale packed to 16 bits as the next MMA's A
+// operand straight from the accumulators, O += P V.
+template <typename T, int D, int GT, bool ASYNC, bool MMA = false>
+__global__ void __launch_bounds__(ATT_THREADS, MMA ? 3 : 1)  // MMA: 3 CTAs / SM (192 KB of ring in flight)
+attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV) {
     using Gm = AttnGeom<T, D>;
     constexpr int VEC = Gm::VEC, LPK = Gm::LPK, KPI = Gm::KPI, TK = Gm::TK, RB = Gm::RB;
+    constexpr int NRED = MMA ? 1 : ATT_CONSUMERS;  // per-warp partial buffers in `red`
+    static_assert(!MMA || (ASYNC && GT == 16 && D == 128 && sizeof(T) == 2 && TK % 32 == 0), "MMA path");
 
-    extern __shared__ __align__(128) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    // the MMA path's TMA swizzle needs 1024-byte aligned stages
+    uint8_t *smem = MMA ? reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                      ~uintptr_t(1023))
+                        : smem_raw;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + ATT_STAGES * Gm::STAGE_BYTES);
     uint64_t *empty = full + ATT_STAGES;
-    float *red = reinterpret_cast<float *>(empty + ATT_STAGES);  // [CONSUMERS][GT][D+2]
+    float *red = reinterpret_cast<float *>(empty + ATT_STAGES);  // [NRED][GT][D+2]
     // join scratch aliases the K/V ring (free once every tile has been consumed)
     float *s_cden = reinterpret_cast<float *>(smem);
     int *s_cviol = reinterpret_cast<int *>(smem) + ATT_MAX_P;
@@ -140,7 +196,7 @@ attn_split_kernel(const AttnArgs args) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < ATT_STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], ATT_CONSUMERS);
+            mbar_init(&empty[s], MMA ? 2 : ATT_CONSUMERS);  // MMA: two warps per stage
         }
         fence_mbar_init();
     }
@@ -160,10 +216,131 @@ attn_split_kernel(const AttnArgs args) {
                 const uint32_t bytes = (uint32_t)n * RB;
                 uint8_t *dk = smem + s * Gm::STAGE_BYTES;
                 uint8_t *dv = dk + TK * RB;
-                mbar_arrive_expect_tx(&full[s], 2 * bytes);
-                bulk_g2s(dk, kbase + (int64_t)key0 * D, bytes, &full[s], kEvictFirst);
-                bulk_g2s(dv, vbase + (int64_t)key0 * D, bytes, &full[s], kEvictFirst);
+                if constexpr (MMA) {
+                    // [2 halves of 64 columns][TK rows][128 B], SWIZZLE_128B; whole boxes
+                    const int row = (int)((int64_t)(b * args.Hkv + kvh) * args.kv_rows_per_head + key0);
+                    mbar_arrive_expect_tx(&full[s], 4 * TK * 128);
+                    tma_load_2d(dk, &tmK, &full[s], 0, row, kEvictFirst);
+                    tma_load_2d(dk + TK * 128, &tmK, &full[s], 64, row, kEvictFirst);
+                    tma_load_2d(dv, &tmV, &full[s], 0, row, kEvictFirst);
+                    tma_load_2d(dv + TK * 128, &tmV, &full[s], 64, row, kEvictFirst);
+                } else {
+                    mbar_arrive_expect_tx(&full[s], 2 * bytes);
+                    bulk_g2s(dk, kbase + (int64_t)key0 * D, bytes, &full[s], kEvictFirst);
+                    bulk_g2s(dv, vbase + (int64_t)key0 * D, bytes, &full[s], kEvictFirst);
+                }
             }
+        }
+    } else if constexpr (MMA) {
+        // ------------------------------------------------ consumer warps, tensor cores
+        // warps 0,1 take the two 16-key slices of even stages, warps 2,3 of odd stages
+        const int r0 = lane >> 2, cq = (lane & 3) * 2;
+        uint32_t qa[D / 16][4];  // Q rows [16 x D] as m16n8k16 A fragments
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int row = r0 + (i & 1) * 8, col = 16 * kk + cq + (i >> 1) * 8;
+                qa[kk][i] = row < gcount
+                                ? *reinterpret_cast<const uint32_t *>(
+                                      static_cast<const T *>(args.q) + (int64_t)b * args.q_sb +
+                                      (int64_t)(h0 + row) * args.q_sh + col)
+                                : 0u;
+            }
+        float o[D / 8][4];
+#pragma unroll
+        for (int nb = 0; nb < D / 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
+        float den0 = 0.f, den1 = 0.f;
+        int viol0 = INT_MAX, viol1 = INT_MAX;
+        const float scale = args.scale, phi = args.phi, ba = args.a, bb = args.b, ps = args.pscale;
+        const int mi = lane >> 3, mr = lane & 7;  // ldmatrix: matrix / row this lane addresses
+        for (int t = warp >> 1; t < ntiles; t += 2) {
+            const int s = t % ATT_STAGES;
+            mbar_wait(&full[s], (t / ATT_STAGES) & 1);
+            const int key0 = k_begin + t * TK;
+            const int n = min(TK, k_end - key0);
+            const uint32_t sk = smem_u32(smem + s * Gm::STAGE_BYTES), sv = sk + TK * RB;
+            for (int k0 = (warp & 1) * 16; k0 < TK; k0 += 32) {
+                if (k0 >= n) break;
+                // S = Q K^T for keys k0 .. k0+15 (two n8 blocks)
+                float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+                {
+                    const int key = k0 + (mi >> 1) * 8 + mr;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const int chunk = 2 * (kk & 3) + (mi & 1);
+                        uint32_t kb[4];
+                        ldsm_x4(kb, sk + (kk >> 2) * TK * 128 + key * 128 + ((chunk ^ (key & 7)) << 4));
+                        mma_16816<T>(sacc[0], qa[kk], kb[0], kb[1]);
+                        mma_16816<T>(sacc[1], qa[kk], kb[2], kb[3]);
+                    }
+                }
+                // unified phi: band check, e^(x - phi) in fp32, P = e * pscale (16-bit)
+                float ep[2][4];
+#pragma unroll
+                for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int key = k0 + 8 * nb + cq + (i & 1);
+                        const float ti = sacc[nb][i] * scale - phi;
+                        const bool valid = key < n, bad = (ti <= ba) || (ti >= bb);
+                        if (valid && bad) {
+                            if (i < 2) viol0 = min(viol0, key0 + key);
+                            else viol1 = min(viol1, key0 + key);
+                        }
+                        const float e = (valid && !bad) ? __expf(ti) : 0.f;
+                        if (i < 2) den0 += e;
+                        else den1 += e;
+                        ep[nb][i] = e * ps;
+                    }
+                const uint32_t pa[4] = {pack2<T>(ep[0][0], ep[0][1]), pack2<T>(ep[0][2], ep[0][3]),
+                                        pack2<T>(ep[1][0], ep[1][1]), pack2<T>(ep[1][2], ep[1][3])};
+                // O += P V
+                {
+                    const int key = k0 + (mi & 1) * 8 + mr;
+#pragma unroll
+                    for (int jj = 0; jj < D / 16; ++jj) {
+                        const int chunk = 2 * (jj & 3) + (mi >> 1);
+                        uint32_t vb[4];
+                        ldsm_x4_t(vb, sv + (jj >> 2) * TK * 128 + key * 128 + ((chunk ^ (key & 7)) << 4));
+                        mma_16816<T>(o[2 * jj], pa, vb[0], vb[1]);
+                        mma_16816<T>(o[2 * jj + 1], pa, vb[2], vb[3]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // rows r0 / r0+8 are shared by the lane quad: fixed butterfly
+#pragma unroll
+        for (int off = 1; off < 4; off <<= 1) {
+            den0 += __shfl_xor_sync(0xffffffffu, den0, off);
+            den1 += __shfl_xor_sync(0xffffffffu, den1, off);
+            viol0 = min(viol0, __shfl_xor_sync(0xffffffffu, viol0, off));
+            viol1 = min(viol1, __shfl_xor_sync(0xffffffffu, viol1, off));
+        }
+        pdl_trigger();  // main stream done: the next kernel may start its prologue
+        // warps add into one [GT][D+2] buffer in fixed order (numerators unscaled exactly)
+        const float ips = args.inv_pscale;
+#pragma unroll 1
+        for (int w = 0; w < ATT_CONSUMERS; ++w) {
+            if (warp == w) {
+#pragma unroll
+                for (int nb = 0; nb < D / 8; ++nb)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        float *dst = red + (r0 + (i >> 1) * 8) * (D + 2) + 8 * nb + cq + (i & 1);
+                        *dst = (w == 0 ? 0.f : *dst) + o[nb][i] * ips;
+                    }
+                if ((lane & 3) == 0) {
+                    float *d0 = red + r0 * (D + 2), *d1 = red + (r0 + 8) * (D + 2);
+                    d0[D] = (w == 0 ? 0.f : d0[D]) + den0;
+                    d1[D] = (w == 0 ? 0.f : d1[D]) + den1;
+                    d0[D + 1] = __int_as_float(w == 0 ? viol0 : min(__float_as_int(d0[D + 1]), viol0));
+                    d1[D + 1] = __int_as_float(w == 0 ? viol1 : min(__float_as_int(d1[D + 1]), viol1));
+                }
+            }
+            named_bar_sync(1, ATT_CONSUMERS * 32);
         }
     } else {
         // ------------------------------------------------ consumer warps
@@ -296,15 +473,15 @@ attn_split_kernel(const AttnArgs args) {
         if (ASYNC) {
             if (e < D) {
                 float s = 0.f;
-                for (int w = 0; w < ATT_CONSUMERS; ++w) s += red[(w * GT + g) * (D + 2) + e];
+                for (int w = 0; w < NRED; ++w) s += red[(w * GT + g) * (D + 2) + e];
                 args.ws_num[slot * D + e] = s;
             } else if (e == D) {
                 float s = 0.f;
-                for (int w = 0; w < ATT_CONSUMERS; ++w) s += red[(w * GT + g) * (D + 2) + D];
+                for (int w = 0; w < NRED; ++w) s += red[(w * GT + g) * (D + 2) + D];
                 args.ws_den[slot] = s;
             } else {
                 int vm = INT_MAX;
-                for (int w = 0; w < ATT_CONSUMERS; ++w)
+                for (int w = 0; w < NRED; ++w)
                     vm = min(vm, __float_as_int(red[(w * GT + g) * (D + 2) + D + 1]));
                 args.ws_viol[slot] = vm;
             }
@@ -335,6 +512,74 @@ attn_split_kernel(const AttnArgs args) {
     if (!s_last) return;
     __threadfence();
 
+    if (ASYNC && !args.viol_index && !args.chunk_num && !args.chunk_den) {
+        // decode hot path (no per-chunk outputs requested): one warp per query
+        // row, all rows of the group in parallel, every partial load of a row
+        // batched (the block-wide join below serialises rows: ~GT x slower at G = 16)
+        const int nsub = args.nsub;
+        for (int g = warp; g < gcount; g += ATT_THREADS / 32) {
+            const int64_t row = row0 + g;
+            const int64_t base = row * P;
+            // chunk verdicts: lane jj owns chunks jj, jj+32, ..; exp-sums in sub order
+            float dpart = 0.f;
+            bool bad = false;
+            for (int jj = lane; jj < args.p; jj += 32) {
+                float cd = 0.f;
+                int vm = INT_MAX;
+                for (int q = 0; q < nsub; ++q) {
+                    const int64_t i = base + (int64_t)jj * nsub + q;
+                    cd += ld_cg_f32(&args.ws_den[i]);
+                    vm = min(vm, __ldcg(&args.ws_viol[i]));
+                }
+                bad |= vm != INT_MAX || !isfinite(cd);  // a non-finite chunk state is a violation
+                dpart += cd;
+            }
+            // numerators: chunk sums in sub order, totals in chunk order
+            constexpr int NDL = (D + 31) / 32;
+            float acc[NDL], cn[NDL];
+#pragma unroll
+            for (int r = 0; r < NDL; ++r) acc[r] = cn[r] = 0.f;
+            constexpr int LBW = 8;
+            for (int i0 = 0; i0 < P; i0 += LBW) {
+                float val[LBW][NDL];
+#pragma unroll
+                for (int q = 0; q < LBW; ++q)
+#pragma unroll
+                    for (int r = 0; r < NDL; ++r) {
+                        const int d = lane + 32 * r;
+                        val[q][r] = (i0 + q < P && d < D) ? ld_cg_f32(&args.ws_num[(base + i0 + q) * D + d]) : 0.f;
+                    }
+#pragma unroll
+                for (int q = 0; q < LBW; ++q) {
+                    if (i0 + q >= P) break;
+#pragma unroll
+                    for (int r = 0; r < NDL; ++r) cn[r] += val[q][r];
+                    if ((i0 + q + 1) % nsub == 0) {  // chunk complete
+#pragma unroll
+                        for (int r = 0; r < NDL; ++r) {
+                            bad |= !isfinite(cn[r]);
+                            acc[r] += cn[r];
+                            cn[r] = 0.f;
+                        }
+                    }
+                }
+            }
+            const bool flagged = __any_sync(0xffffffffu, bad) != 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dpart += __shfl_xor_sync(0xffffffffu, dpart, o);
+            if (lane == 0) {
+                args.row_flags[row] = flagged ? 1 : 0;
+                if (flagged && args.rows_recomputed) atomicAdd(args.rows_recomputed, 1);
+            }
+            if (!flagged) {
+                T *op = static_cast<T *>(args.o) + (int64_t)b * args.o_sb + (int64_t)(h0 + g) * args.o_sh;
+#pragma unroll
+                for (int r = 0; r < NDL; ++r)
+                    if (lane + 32 * r < D) op[lane + 32 * r] = Elem<T>::from_f(acc[r] / dpart);
+            }
+        }
+        return;
+    }
     constexpr int LB = 32;  // partial loads kept in flight per thread
     for (int g = 0; g < gcount; ++g) {
         const int64_t row = row0 + g;
@@ -465,10 +710,42 @@ attn_split_kernel(const AttnArgs args) {
 // ---------------------------------------------------------------------- host
 struct AttnLayout {
     int G, GT, n_rg, p, nsub, P;
+    bool mma;      // async launch on tensor cores (GQA/MQA): 16-row groups
+    int n_rg_mma;  // its row groups per kv head
+    float pscale;  // its power-of-two P scale
     size_t off_num, off_den, off_m, off_viol, off_cnt, total;
 };
 
 static int pick_gt(int G) { return G >= 8 ? 8 : G >= 4 ? 4 : G >= 2 ? 2 : 1; }
+
+// Tensor-core async path: GQA/MQA groups (G >= 4) at D = 128 in f16/bf16 over a
+// contiguous [B, Hkv, Lmax, D] cache.  f16 P needs the band's dynamic range
+// e^(b - a) inside fp16's normal range with margin ((b - a) log2 e <= 28);
+// P is scaled by 2^(14 - ceil(b log2 e)) so e^b lands below 2^14.
+// FDPP_ATTN_MMA=0 forces the CUDA-core path.
+static bool mma_enabled() {
+    static int v = [] {
+        const char *e = getenv("FDPP_ATTN_MMA");
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+static bool mma_eligible(const fdpp_attn_params *p, int G, float *pscale) {
+    if (!mma_enabled() || p->mode != FDPP_ATTN_ASYNC || G < 4 || p->D != 128) return false;
+    if (p->dtype != FDPP_F16 && p->dtype != FDPP_BF16) return false;
+    if (p->kv_stride_h % p->D != 0 || p->kv_stride_b != (int64_t)p->Hkv * p->kv_stride_h ||
+        p->kv_stride_h < (int64_t)p->L * p->D)
+        return false;
+    const double log2e = 1.4426950408889634;
+    if (p->dtype == FDPP_F16) {
+        if (!(p->b > p->a) || (double)(p->b - p->a) * log2e > 28.0) return false;
+        *pscale = ldexpf(1.f, 14 - (int)ceil((double)p->b * log2e));
+    } else {
+        *pscale = 1.f;
+    }
+    return true;
+}
 
 static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
     FDPP_REQUIRE(p != nullptr, FDPP_ERR_VALUE, "null params");
@@ -478,25 +755,38 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
     lay->G = p->Hq / p->Hkv;
     lay->GT = pick_gt(lay->G);
     lay->n_rg = (lay->G + lay->GT - 1) / lay->GT;
-    const int groups = p->B * p->Hkv * lay->n_rg;
+    const int groups = p->B * p->Hkv * lay->n_rg;  // counters (the CUDA-core grouping is the finest)
+    lay->pscale = 1.f;
+    lay->mma = mma_eligible(p, lay->G, &lay->pscale);
+    lay->n_rg_mma = (lay->G + 15) / 16;
+    const int launch_groups = lay->mma ? p->B * p->Hkv * lay->n_rg_mma : groups;
     const int sms = sm_count() > 0 ? sm_count() : 148;
     if (p->p > 0) {
         FDPP_REQUIRE(p->p <= p->L, FDPP_ERR_VALUE, "partition count must be in [1, %d], got %d",
                      p->L, p->p);
         FDPP_REQUIRE(p->p <= ATT_MAX_P, FDPP_ERR_VALUE, "partition count above %d", ATT_MAX_P);
         lay->p = p->p;
+    } else if (lay->mma) {
+        // auto, tensor-core path: ~2 CTAs per SM in one wave, >= 512 keys each
+        // (fewer, longer CTAs amortise the per-CTA ramp: profiles/r1_attn_gqa_sweep.txt)
+        int want = (2 * sms + launch_groups - 1) / launch_groups;
+        int maxp = p->L / 512 > 0 ? p->L / 512 : 1;
+        lay->p = want < 1 ? 1 : (want > maxp ? maxp : want);
+        if (lay->p > ATT_MAX_P) lay->p = ATT_MAX_P;
     } else {
         // auto: enough chunks for ~8 CTAs per SM over the launch, >= 512 keys each
-        int want = (8 * sms + groups - 1) / groups;
+        int want = (8 * sms + launch_groups - 1) / launch_groups;
         int maxp = p->L / 512 > 0 ? p->L / 512 : 1;
         lay->p = want < 1 ? 1 : (want > maxp ? maxp : want);
         if (lay->p > ATT_MAX_P) lay->p = ATT_MAX_P;
     }
     if (p->splits_per_chunk > 0) {
         lay->nsub = p->splits_per_chunk;
+    } else if (lay->mma) {
+        lay->nsub = 1;
     } else {
         const int per_chunk = p->L / lay->p;
-        int want = (8 * sms + groups * lay->p - 1) / (groups * lay->p);
+        int want = (8 * sms + launch_groups * lay->p - 1) / (launch_groups * lay->p);
         int maxs = per_chunk / 512 > 0 ? per_chunk / 512 : 1;  // >= 512 keys per CTA
         lay->nsub = want < 1 ? 1 : (want > maxs ? maxs : want);
     }
@@ -516,12 +806,15 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
     return FDPP_OK;
 }
 
-template <typename T, int D, int GT, bool ASYNC>
-static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st) {
+template <typename T, int D, int GT, bool ASYNC, bool MMA = false>
+static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st,
+                               const CUtensorMap *tmK = nullptr, const CUtensorMap *tmV = nullptr) {
     using Gm = AttnGeom<T, D>;
-    const int smem = ATT_STAGES * Gm::STAGE_BYTES + 2 * ATT_STAGES * 8 +
-                     ATT_CONSUMERS * GT * (D + 2) * (int)sizeof(float);
-    auto kern = attn_split_kernel<T, D, GT, ASYNC>;
+    const int smem = (MMA ? 1024 : 0) + ATT_STAGES * Gm::STAGE_BYTES + 2 * ATT_STAGES * 8 +
+                     (MMA ? 1 : ATT_CONSUMERS) * GT * (D + 2) * (int)sizeof(float);
+    auto kern = attn_split_kernel<T, D, GT, ASYNC, MMA>;
+    CUtensorMap none;
+    memset(&none, 0, sizeof(none));
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -529,7 +822,8 @@ static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st) {
         attr = true;
     }
     dim3 grid(grid_x, a.Hkv * a.n_rg, a.B);
-    cudaError_t e = launch_kernel(kern, grid, dim3(ATT_THREADS), smem, st, a);
+    cudaError_t e = launch_kernel(kern, grid, dim3(ATT_THREADS), smem, st, a, tmK ? *tmK : none,
+                                  tmV ? *tmV : none);
     if (e != cudaSuccess) return cuda_status(e, "attn_split_kernel launch");
     return FDPP_OK;
 }
@@ -562,6 +856,12 @@ static fdpp_status by_d(const AttnArgs &a, int D, int gt, int gx, cudaStream_t s
     }
     set_error("unsupported head dim %d for this dtype (pad D to a power of two >= 16 bytes)", D);
     return FDPP_ERR_UNSUPPORTED;
+}
+
+static fdpp_status launch_mma(const AttnArgs &a, int dtype, int gx, const CUtensorMap *tmK,
+                              const CUtensorMap *tmV, cudaStream_t st) {
+    return dtype == FDPP_BF16 ? launch_attn<__nv_bfloat16, 128, 16, true, true>(a, gx, st, tmK, tmV)
+                              : launch_attn<__half, 128, 16, true, true>(a, gx, st, tmK, tmV);
 }
 
 template <bool ASYNC>
@@ -640,7 +940,21 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
         return by_dtype<false>(a, p->dtype, p->D, lay.GT, lay.P, st);
     }
     a.only_flagged = false;
-    s = by_dtype<true>(a, p->dtype, p->D, lay.GT, lay.P, st);
+    if (lay.mma) {
+        // 2-D maps over the cache as [B * Hkv * Lmax rows, D]: 32-row x 64-column boxes
+        CUtensorMap mk, mv;
+        const int64_t rows = (int64_t)p->B * p->Hkv * (p->kv_stride_h / p->D);
+        if ((s = make_kmajor_map(&mk, p->k, rows, p->D, p->D, 32, p->dtype)) != FDPP_OK) return s;
+        if ((s = make_kmajor_map(&mv, p->v, rows, p->D, p->D, 32, p->dtype)) != FDPP_OK) return s;
+        AttnArgs am = a;
+        am.n_rg = lay.n_rg_mma;
+        am.pscale = lay.pscale;
+        am.inv_pscale = 1.f / lay.pscale;
+        am.kv_rows_per_head = p->kv_stride_h / p->D;
+        s = launch_mma(am, p->dtype, lay.P, &mk, &mv, st);
+    } else {
+        s = by_dtype<true>(a, p->dtype, p->D, lay.GT, lay.P, st);
+    }
     if (s != FDPP_OK) return s;
     // synchronized recompute of flagged rows (attention.py:283-285), always launched
     a.only_flagged = true;

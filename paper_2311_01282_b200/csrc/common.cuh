@@ -81,6 +81,12 @@ inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, 
     return launch_kernel_cluster(kern, grid, block, smem, st, 1, std::forward<Args>(args)...);
 }
 
+// 2-D tile map over a row-major [rows, cols] 16-bit matrix (leading dim ld):
+// box = [64 cols x box_rows], SWIZZLE_128B, OOB zero-filled; cached per
+// (pointer, shape).  Defined in gemm.cu.
+fdpp_status make_kmajor_map(CUtensorMap *out, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
+                            int box_rows, int dtype);
+
 // ------------------------------------------------------------- element types
 template <typename T> struct Elem;
 template <> struct Elem<__half> {

@@ -907,8 +907,8 @@ struct MapKeyHash {
 
 // 2-D K-major tile map over a row-major [rows, cols] matrix (leading dim ld),
 // box = [box_rows x 64] elements, SWIZZLE_128B, OOB rows/cols zero-filled.
-static fdpp_status make_kmajor_map(CUtensorMap *out, const void *ptr, int64_t rows, int64_t cols,
-                                   int64_t ld, int box_rows, int dtype) {
+fdpp_status make_kmajor_map(CUtensorMap *out, const void *ptr, int64_t rows, int64_t cols,
+                            int64_t ld, int box_rows, int dtype) {
     static std::mutex mu;
     static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
     MapKey key{ptr, rows, cols, ld, box_rows, dtype};

@@ -16,7 +16,7 @@ for B, Hq, Hkv, L in ((8, 32, 2, 32768), (8, 32, 2, 4096), (32, 64, 8, 1024), (8
     q = torch.randn((B, Hq, D), device="cuda").half()
     out = torch.empty_like(q)
     byt = B * Hkv * L * D * 4 + 2 * B * Hq * D * 2
-    for p, spc in ((0, 0), (8, 0), (16, 0), (32, 0), (64, 0)):
+    for p, spc in ((0, 0), (16, 1), (18, 1), (19, 1), (20, 1), (32, 1), (37, 1)):
         cfg = fd.AttentionConfig(p=p, scale=1 / math.sqrt(D), calib=cal, splits_per_chunk=spc)
         plan = fd.attention.plan(q, k, cfg)
         med, _ = median_mad(measure(lambda: fd.decode_attention(q, k, v, cfg, "async", out=out), reps=10, warmup=2))
