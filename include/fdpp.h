@@ -207,6 +207,12 @@ fdpp_status fdpp_silu_mul(const void *gu, void *out, int32_t rows, int32_t F, in
  * one-tile row sums a fused RMSNorm prologue consumes). */
 fdpp_status fdpp_embed(const int32_t *ids, const void *table, void *out, int32_t B, int32_t dim,
                        float *ssq_out, int32_t dtype, void *stream);
+
+/* Per-row sum of squares of x[B, dim] into ssq_out[B] (one tile per row): the
+ * folded-RMSNorm input of the next projection after a tensor-parallel
+ * all-reduce of the residual stream. */
+fdpp_status fdpp_row_ssq(const void *x, float *ssq_out, int32_t B, int32_t dim, int32_t dtype,
+                         void *stream);
 /* ids[r] = argmax_j logits[r, j] (lowest index on ties). */
 fdpp_status fdpp_argmax(const void *logits, int32_t *ids, int32_t rows, int32_t vocab,
                         int32_t dtype, void *stream);

@@ -87,6 +87,7 @@ SIGNATURES = {
                                  c_i64, c_i64, c_f32, c_i32, c_vp]),
     "fdpp_silu_mul": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_embed": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_i32, c_vp]),
+    "fdpp_row_ssq": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_argmax": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_advance_positions": (c_i32, [c_vp, c_vp, c_i32, c_vp]),
 }

@@ -109,6 +109,30 @@ __global__ void embed_kernel(const int32_t *__restrict__ ids, const T *__restric
     }
 }
 
+// Per-row sum of squares of the residual stream (one tile spanning the row):
+// what the folded-RMSNorm prologue of the next projection needs after a
+// tensor-parallel all-reduce (the single-GPU path gets it from GEMM epilogues).
+template <typename T>
+__global__ void row_ssq_kernel(const T *__restrict__ x, int dim, float *__restrict__ ssq_out) {
+    pdl_wait();
+    pdl_trigger();
+    const int b = blockIdx.x;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < dim; i += blockDim.x) {
+        const float f = Elem<T>::to_f(x[(int64_t)b * dim + i]);
+        ss = fmaf(f, f, ss);
+    }
+    __shared__ float red[32];
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];  // warp order
+        ssq_out[b] = t;
+    }
+}
+
 template <typename T>
 __global__ void argmax_kernel(const T *__restrict__ logits, int32_t *__restrict__ ids, int vocab) {
     pdl_wait();
@@ -207,6 +231,18 @@ extern "C" fdpp_status fdpp_embed(const int32_t *ids, const void *table, void *o
                                             static_cast<const T *>(table), static_cast<T *>(out),
                                             (int)dim, ssq_out));
     if (e != cudaSuccess) return cuda_status(e, "embed_kernel launch");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_row_ssq(const void *x, float *ssq_out, int32_t B, int32_t dim, int32_t dtype,
+                                    void *stream) {
+    FDPP_REQUIRE(x && ssq_out, FDPP_ERR_VALUE, "null pointer");
+    FDPP_REQUIRE(B >= 1 && dim >= 1, FDPP_ERR_SHAPE, "row_ssq dims");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaSuccess;
+    FDPP_DT_SWITCH(dtype, e = launch_kernel(row_ssq_kernel<T>, dim3(B), dim3(256), 0, st,
+                                            static_cast<const T *>(x), (int)dim, ssq_out));
+    if (e != cudaSuccess) return cuda_status(e, "row_ssq_kernel launch");
     return FDPP_OK;
 }
 

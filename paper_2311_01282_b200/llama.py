@@ -27,7 +27,7 @@ from dataclasses import dataclass
 
 import torch
 
-from . import _lib, workspace
+from . import _lib, tp as _tp, workspace
 from . import dispatch as _dispatch_mod  # noqa: F401  (module, not the function)
 from .attention import AttentionConfig, decode_attention
 from .gemm import PackedWeight, run_fused
@@ -55,19 +55,18 @@ class LlamaConfig:
     rope_theta: float = 10000.0
     eps: float = 1e-5
 
-    def gemm_shapes(self):
-        """[N, K] of each dispatched GEMM in one step."""
-        qkv = (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
-        return {"qkv": (qkv, self.hidden), "o": (self.hidden, self.n_heads * self.head_dim),
-                "gate_up": (2 * self.ffn, self.hidden), "down": (self.hidden, self.ffn),
-                "lm_head": (self.vocab, self.hidden)}
+    def gemm_shapes(self, tp: int = 1):
+        """[N, K] of each dispatched GEMM in one step (on one of `tp` ranks)."""
+        return _tp.rank_gemm_shapes(self, tp)
 
-    def weight_bytes(self, dtype_bytes=2) -> int:
-        per_layer = sum(n * k for n, k in list(self.gemm_shapes().values())[:4]) + 2 * self.hidden
+    def weight_bytes(self, dtype_bytes=2, tp: int = 1) -> int:
+        """Bytes one rank streams per step (sharded projections + replicated
+        embedding row reads are negligible; LM head replicated)."""
+        per_layer = sum(n * k for n, k in list(self.gemm_shapes(tp).values())[:4]) + 2 * self.hidden
         return dtype_bytes * (self.n_layers * per_layer + 2 * self.vocab * self.hidden + self.hidden)
 
-    def kv_bytes_per_token(self, dtype_bytes=2) -> int:
-        return 2 * self.n_layers * self.n_kv_heads * self.head_dim * dtype_bytes
+    def kv_bytes_per_token(self, dtype_bytes=2, tp: int = 1) -> int:
+        return 2 * self.n_layers * (self.n_kv_heads // tp) * self.head_dim * dtype_bytes
 
 
 LLAMA2_7B = LlamaConfig("llama2-7b", 4096, 32, 32, 128, 11008, 32, 32000)
@@ -76,10 +75,10 @@ CHATGLM2_6B = LlamaConfig("chatglm2-6b", 4096, 32, 2, 128, 13696, 28, 65024)
 
 
 def build_dispatch_table(cfg: LlamaConfig, m_sweep=D.B200_M_SWEEP, reps=5, dtype=torch.float16,
-                         fingerprint=None):
+                         fingerprint=None, tp: int = 1):
     """Profile every GEMM shape of a decode step on this device (profile_shape)."""
     table = D.DispatchTable(fingerprint=fingerprint or D.default_fingerprint())
-    for n, k in sorted(set(cfg.gemm_shapes().values())):
+    for n, k in sorted(set(cfg.gemm_shapes(tp).values())):
         table.add(D.profile_shape(n, k, m_sweep=m_sweep, reps=reps, dtype=dtype))
     return table
 
@@ -101,32 +100,58 @@ class LlamaDecoder:
 
     def __init__(self, cfg: LlamaConfig, batch: int, max_len: int, *, table=None,
                  calib: ScalingCalibration = GOLDEN_CALIB, dtype=torch.float16, seed: int = 0,
-                 attn_p: int = 0, attn_splits: int = 0, n_layers: int = None, fused: bool = True):
+                 attn_p: int = 0, attn_splits: int = 0, n_layers: int = None, fused: bool = True,
+                 tp_rank: int = 0, tp_size: int = 1, group=None, weights: dict = None):
+        """tp_size > 1: this process is rank tp_rank of a tensor-parallel group
+        (tp.py): sharded QKV / O / gate|up / down, local heads and KV cache, one
+        NCCL all-reduce of the residual stream after O and after down (captured
+        in the step's CUDA graph).  weights: optional FULL model weights
+        {"layers": [{qkv, o, gate_up, down ([N, K]), ln1, ln2}], "embed",
+        "lm_head" ([vocab, hidden]), "ln_f"} to shard; default random init."""
         _lib.require_cuda()
         self.cfg, self.B, self.max_len, self.dtype = cfg, batch, max_len, dtype
         self.n_layers = n_layers or cfg.n_layers
+        self.tp_rank, self.tp_size, self.group = tp_rank, tp_size, group
+        sd = _tp.shard_dims(cfg, tp_size)
         dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
-        g = torch.Generator(device=dev).manual_seed(seed)
-        shapes = cfg.gemm_shapes()
+        g = torch.Generator(device=dev).manual_seed(seed + 7919 * tp_rank)   # sharded tensors
+        g_rep = torch.Generator(device=dev).manual_seed(seed)                # replicated tensors
+        shapes = cfg.gemm_shapes(tp_size)
 
-        def w(n, k):
+        def w(n, k, gen=g):
             t = torch.empty((n, k), dtype=dtype, device=dev)
-            t.normal_(0.0, 1.0 / math.sqrt(k), generator=g)
+            t.normal_(0.0, 1.0 / math.sqrt(k), generator=gen)
             return PackedWeight(t, k, n)
 
+        def packed(t):
+            t = t.to(device=dev, dtype=dtype).contiguous()
+            return PackedWeight(t, t.shape[1], t.shape[0])
+
         self.layers = []
-        for _ in range(self.n_layers):
+        for li in range(self.n_layers):
+            if weights is not None:
+                Ls = _tp.shard_layer(weights["layers"][li], cfg, tp_rank, tp_size)
+                self.layers.append({k: packed(Ls[k]) for k in ("qkv", "o", "gate_up", "down")} |
+                                   {k: Ls[k].to(device=dev, dtype=dtype) for k in ("ln1", "ln2")})
+                continue
             self.layers.append({
                 "qkv": w(*shapes["qkv"]), "o": w(*shapes["o"]),
                 "gate_up": w(*shapes["gate_up"]), "down": w(*shapes["down"]),
                 "ln1": torch.ones(cfg.hidden, dtype=dtype, device=dev),
                 "ln2": torch.ones(cfg.hidden, dtype=dtype, device=dev),
             })
-        self.embed = torch.empty((cfg.vocab, cfg.hidden), dtype=dtype, device=dev).normal_(0, 1, generator=g)
-        self.lm_head = w(*shapes["lm_head"])
-        self.ln_f = torch.ones(cfg.hidden, dtype=dtype, device=dev)
-        Hq, Hkv, Dh = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+        if weights is not None:
+            self.embed = weights["embed"].to(device=dev, dtype=dtype).contiguous()
+            self.lm_head = packed(weights["lm_head"])
+            self.ln_f = weights["ln_f"].to(device=dev, dtype=dtype)
+        else:
+            self.embed = torch.empty((cfg.vocab, cfg.hidden), dtype=dtype, device=dev).normal_(
+                0, 1, generator=g_rep)
+            self.lm_head = w(*shapes["lm_head"], gen=g_rep)
+            self.ln_f = torch.ones(cfg.hidden, dtype=dtype, device=dev)
+        Hq, Hkv, Dh = sd.n_heads, sd.n_kv_heads, cfg.head_dim
+        self.n_heads_local, self.n_kv_heads_local = Hq, Hkv
         self.k_cache = [torch.empty((batch, Hkv, max_len, Dh), dtype=dtype, device=dev)
                         for _ in range(self.n_layers)]
         self.v_cache = [torch.empty_like(self.k_cache[0]) for _ in range(self.n_layers)]
@@ -136,8 +161,9 @@ class LlamaDecoder:
         self.qkv = torch.zeros((B, shapes["qkv"][0]), dtype=dtype, device=dev)
         self.q = torch.zeros((B, Hq, Dh), dtype=dtype, device=dev)
         self.attn = torch.zeros((B, Hq, Dh), dtype=dtype, device=dev)
-        self.gu = torch.zeros((B, 2 * cfg.ffn), dtype=dtype, device=dev)
-        self.act = torch.zeros((B, cfg.ffn), dtype=dtype, device=dev)
+        self.ffn_local = sd.ffn
+        self.gu = torch.zeros((B, 2 * sd.ffn), dtype=dtype, device=dev)
+        self.act = torch.zeros((B, sd.ffn), dtype=dtype, device=dev)
         self.logits = torch.zeros((B, cfg.vocab), dtype=dtype, device=dev)
         self.ids = torch.zeros(B, dtype=torch.int32, device=dev)
         self.pos = torch.zeros(B, dtype=torch.int32, device=dev)
@@ -155,12 +181,14 @@ class LlamaDecoder:
         self.attn_cfg = AttentionConfig(p=attn_p, scale=1.0 / math.sqrt(Dh), calib=calib,
                                         splits_per_chunk=attn_splits)
         if table is None:
-            table = build_dispatch_table(cfg, dtype=dtype)
+            table = build_dispatch_table(cfg, dtype=dtype, tp=tp_size)
         self.table = table
         self.choices = {op: D.dispatch(B, n, k, table) for op, (n, k) in shapes.items()}
         # the fused step is built on ImplB (prologue/epilogue fusions); use it when
         # the dispatch table picks ImplB for every projection at this batch
         fused = fused and all(c == D.KernelChoice.IMPL_B for c in self.choices.values())
+        if tp_size > 1 and not fused:
+            raise NotImplementedError("tensor parallelism runs on the fused (ImplB) decode step")
         self.graph = None
         if fused:  # fold the RMSNorm weights into the following projections' columns
             for L in self.layers:
@@ -168,9 +196,10 @@ class LlamaDecoder:
                 L["gate_up_f"] = fold_norm(L["gate_up"], L["ln2"])
             self.lm_head_f = fold_norm(self.lm_head, self.ln_f)
         self.fused = fused
-        # fused: embed + L x (qkv+rope, attn async, attn recompute, o, gate_up, silu, down)
-        #        + lm_head + argmax + advance
-        self.launches_per_step = (1 + self.n_layers * 7 + 3) if fused else (1 + self.n_layers * 10 + 4)
+        # fused: embed + L x (qkv+rope, attn async, attn recompute, o, gate_up, silu, down
+        #        [+ 2 row-ssq after the all-reduces]) + lm_head + argmax + advance
+        per_layer = 7 + (2 if tp_size > 1 else 0)
+        self.launches_per_step = (1 + self.n_layers * per_layer + 3) if fused else (1 + self.n_layers * 10 + 4)
 
     # ------------------------------------------------------------------ state
     def prefill_random(self, L: int, seed: int = 1):
@@ -205,7 +234,18 @@ class LlamaDecoder:
         cfg, B, dt = self.cfg, self.B, _lib.dtype_code(self.dtype)
         lib = _lib.load()
         st = _lib.stream_handle()
-        Hq, Dh = cfg.n_heads, cfg.head_dim
+        Hq, Dh = self.n_heads_local, cfg.head_dim
+        tp = self.tp_size > 1
+        lead = self.tp_rank == 0  # the rank whose row-parallel epilogue adds the residual
+
+        def all_reduce_x(ssq):
+            # x = sum over ranks of (x + partial_0, partial_1, ...); then the
+            # next projection's folded-RMSNorm input (one tile per row)
+            import torch.distributed as dist
+            dist.all_reduce(self.x, group=self.group)
+            _lib.check(lib.fdpp_row_ssq(self.x.data_ptr(), ssq.data_ptr(), B, cfg.hidden, dt,
+                                        _lib.stream_handle()), "row_ssq")
+
         _lib.check(lib.fdpp_embed(self.ids.data_ptr(), self.embed.data_ptr(), self.x.data_ptr(), B,
                                   cfg.hidden, self.ssq_a.data_ptr(), dt, st), "embed")
         ssq_tiles = 1
@@ -217,15 +257,19 @@ class LlamaDecoder:
                             "theta": cfg.rope_theta})
             decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
                              seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed)
-            run_fused(self.attn.view(B, Hq * Dh), L["o"], out=self.x, residual=self.x,
-                      ssq_out=self.ssq_b, ws_tag="decode_gemm")
+            run_fused(self.attn.view(B, Hq * Dh), L["o"], out=self.x, residual=self.x if lead else None,
+                      ssq_out=None if tp else self.ssq_b, ws_tag="decode_gemm")
+            if tp:
+                all_reduce_x(self.ssq_b)
             run_fused(self.x, L["gate_up_f"], out=self.gu, x_op=3, ssq_in=self.ssq_b,
-                      ssq_tiles=self.ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
-            _lib.check(lib.fdpp_silu_mul(self.gu.data_ptr(), self.act.data_ptr(), B, cfg.ffn, dt, st),
-                       "silu_mul")
-            run_fused(self.act, L["down"], out=self.x, residual=self.x, ssq_out=self.ssq_a,
-                      ws_tag="decode_gemm")
-            ssq_tiles = self.ssq_tiles
+                      ssq_tiles=1 if tp else self.ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
+            _lib.check(lib.fdpp_silu_mul(self.gu.data_ptr(), self.act.data_ptr(), B, self.ffn_local, dt,
+                                         st), "silu_mul")
+            run_fused(self.act, L["down"], out=self.x, residual=self.x if lead else None,
+                      ssq_out=None if tp else self.ssq_a, ws_tag="decode_gemm")
+            if tp:
+                all_reduce_x(self.ssq_a)
+            ssq_tiles = 1 if tp else self.ssq_tiles
         run_fused(self.x, self.lm_head_f, out=self.logits, x_op=3, ssq_in=self.ssq_a,
                   ssq_tiles=ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
         _lib.check(lib.fdpp_argmax(self.logits.data_ptr(), self.ids.data_ptr(), B, cfg.vocab, dt, st),
@@ -237,7 +281,7 @@ class LlamaDecoder:
         cfg, B, dt = self.cfg, self.B, _lib.dtype_code(self.dtype)
         lib = _lib.load()
         st = _lib.stream_handle()
-        Hq, Hkv, Dh = cfg.n_heads, cfg.n_kv_heads, cfg.head_dim
+        Hq, Hkv, Dh = self.n_heads_local, self.n_kv_heads_local, cfg.head_dim
         _lib.check(lib.fdpp_embed(self.ids.data_ptr(), self.embed.data_ptr(), self.x.data_ptr(), B,
                                   cfg.hidden, None, dt, st), "embed")
         for li, L in enumerate(self.layers):
@@ -255,7 +299,7 @@ class LlamaDecoder:
             _lib.check(lib.fdpp_rmsnorm(self.x.data_ptr(), L["ln2"].data_ptr(), self.h.data_ptr(), B,
                                         cfg.hidden, cfg.eps, dt, st), "rmsnorm")
             self._gemm("gate_up", self.h, L["gate_up"], self.gu)
-            _lib.check(lib.fdpp_silu_mul(self.gu.data_ptr(), self.act.data_ptr(), B, cfg.ffn, dt, st),
+            _lib.check(lib.fdpp_silu_mul(self.gu.data_ptr(), self.act.data_ptr(), B, self.ffn_local, dt, st),
                        "silu_mul")
             self._gemm("down", self.act, L["down"], self.x, residual=self.x)
         _lib.check(lib.fdpp_rmsnorm(self.x.data_ptr(), self.ln_f.data_ptr(), self.h.data_ptr(), B,

@@ -138,3 +138,64 @@ def test_fused_step_matches_unfused_step(torch, mods):
     a.step()
     torch.cuda.synchronize()
     assert torch.equal(a.pos, s0 + 1)
+
+
+def _tiny_weights(torch, cfg, seed=0):
+    g = torch.Generator().manual_seed(seed)
+
+    def w(n, k):
+        return torch.randn((n, k), generator=g) / math.sqrt(k)
+
+    D = cfg.head_dim
+    layers = [{"qkv": w((cfg.n_heads + 2 * cfg.n_kv_heads) * D, cfg.hidden),
+               "o": w(cfg.hidden, cfg.n_heads * D), "gate_up": w(2 * cfg.ffn, cfg.hidden),
+               "down": w(cfg.hidden, cfg.ffn),
+               "ln1": 1 + 0.1 * torch.randn(cfg.hidden, generator=g),
+               "ln2": 1 + 0.1 * torch.randn(cfg.hidden, generator=g)} for _ in range(cfg.n_layers)]
+    return {"layers": layers, "embed": torch.randn((cfg.vocab, cfg.hidden), generator=g),
+            "lm_head": w(cfg.vocab, cfg.hidden), "ln_f": 1 + 0.1 * torch.randn(cfg.hidden, generator=g)}
+
+
+@pytest.mark.parametrize("n_kv", [4, 1])  # MHA-style CUDA-core attention; G = 8 tensor-core attention
+def test_decode_step_matches_fp32_reference(torch, mods, n_kv):
+    """The whole fused decode step (folded RMSNorm, RoPE + KV append epilogue,
+    async attention, residual epilogues, SiLU*up) against tp.reference_layer
+    in fp32 on the same weights, KV state and tokens."""
+    from paper_2311_01282_b200 import tp
+    fd, _lib, gemm, llama, D = mods
+    cfg = llama.LlamaConfig("tiny", hidden=1024, n_heads=8, n_kv_heads=n_kv, head_dim=128, ffn=1536,
+                            n_layers=2, vocab=512)
+    W = _tiny_weights(torch, cfg)
+    table = D.DispatchTable(fingerprint="test")
+    for n, k in cfg.gemm_shapes().values():
+        table.add(D.DispatchEntry(n=n, k=k, m1=1, m2=128))
+    B, L = 4, 200
+    dec = llama.LlamaDecoder(cfg, B, L + 8, table=table, weights=W)
+    assert dec.fused
+    dec.prefill_random(L, seed=3)
+    x = W["embed"][dec.ids.long().cpu()].half().float()
+    kc = [k.float().cpu() for k in dec.k_cache]
+    vc = [v.float().cpu() for v in dec.v_cache]
+    pos = dec.pos.long().cpu()
+    for li in range(cfg.n_layers):
+        Lw = {k: (v.half().float() if k in ("qkv", "o", "gate_up", "down") else v.half().float())
+              for k, v in W["layers"][li].items()}
+        x = tp.reference_layer(x, Lw, kc[li], vc[li], pos, pos + 1, cfg, cfg.n_heads, cfg.n_kv_heads)
+    dec.enqueue_step()
+    torch.cuda.synchronize()
+    assert int(dec.recomputed.item()) == 0
+    assert _rel(dec.x, x) <= 2e-2
+    for li in range(cfg.n_layers):  # appended K rows (RoPE'd in the QKV epilogue)
+        got = dec.k_cache[li][torch.arange(B), :, pos.cuda()].float().cpu()
+        exp = kc[li][torch.arange(B), :, pos]
+        assert _rel(got, exp) <= 2e-2
+
+
+def test_row_ssq(torch, mods):
+    fd, _lib, *_ = mods
+    x = torch.randn((5, 4096), device="cuda").half()
+    out = torch.empty(5, device="cuda")
+    _lib.check(_lib.load().fdpp_row_ssq(x.data_ptr(), out.data_ptr(), 5, 4096, 0, _lib.stream_handle()))
+    torch.cuda.synchronize()
+    ref = (x.float() ** 2).sum(1)
+    assert torch.allclose(out, ref, rtol=1e-5)
