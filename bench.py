@@ -95,7 +95,7 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- CPU leg
-def cpu_reference_step(B, L, cfg, rng_seed=0, head_sample=8):
+def cpu_reference_step(B, L, cfg, rng_seed=0, head_sample=8, n_frac=1):
     """One bounded sample of the reference's CPU path for the workload: the
     dispatched GEMMs of ONE decoder layer at M = B (ImplA, the reference's
     dispatched kernel on CPU at every M <= 64) plus async
@@ -109,19 +109,22 @@ def cpu_reference_step(B, L, cfg, rng_seed=0, head_sample=8):
     rng = np.random.default_rng(rng_seed)
     shapes = cfg.gemm_shapes()
     t_gemm = 0.0
+    # ImplA's cost is linear in N: a 1/n_frac column slice, scaled back up
     for op in ("qkv", "o", "gate_up", "down"):
         n, k = shapes[op]
+        n = max(1, n // n_frac)
         a = rng.standard_normal((B, k), dtype=np.float32)
         b = rng.standard_normal((k, n), dtype=np.float32)
         t0 = time.perf_counter()
         O.impl_a_gemv(a, b)
-        t_gemm += time.perf_counter() - t0
+        t_gemm += (time.perf_counter() - t0) * n_frac
     n, k = shapes["lm_head"]
+    n = max(1, n // n_frac)
     a = rng.standard_normal((B, k), dtype=np.float32)
     b = rng.standard_normal((k, n), dtype=np.float32)
     t0 = time.perf_counter()
     O.impl_a_gemv(a, b)
-    t_head = time.perf_counter() - t0
+    t_head = (time.perf_counter() - t0) * n_frac
     Dh = cfg.head_dim
     calib = O.Calib(-7.775933742523193, -1.0, 16.577659606933594)
     K = rng.standard_normal((L, Dh), dtype=np.float32)
@@ -133,7 +136,8 @@ def cpu_reference_step(B, L, cfg, rng_seed=0, head_sample=8):
     t_head_attn = (time.perf_counter() - t0) / head_sample
     t_attn = t_head_attn * B * cfg.n_heads
     t_step = cfg.n_layers * (t_gemm + t_attn) + t_head
-    desc = (f"1 decoder layer (4 ImplA GEMMs at M={B}) + async attention on {head_sample} "
+    sl = f" on 1/{n_frac} of their columns" if n_frac > 1 else ""
+    desc = (f"1 decoder layer (4 ImplA GEMMs at M={B}{sl}) + async attention on {head_sample} "
             f"(batch, head) pairs at L={L}, p=4, extrapolated x{cfg.n_layers} layers + LM head; "
             f"oracle C port of the reference's numba kernels, {cores} threads")
     return t_step, desc, cores
@@ -163,6 +167,77 @@ def _op_graph_time(torch, fn, reps):
     return e0.elapsed_time(e1) * 1e-3 / reps
 
 
+MODELS = {"llama2-7b": "LLAMA2_7B", "chatglm2-6b": "CHATGLM2_6B", "llama2-70b": "LLAMA2_70B"}
+
+
+def _load_table(D, cfg, tp):
+    """The committed B200 dispatch table (tools/make_table.py); shapes it lacks
+    get the measured B200 policy for M <= 64 (ImplB from M = 1, ImplC beyond:
+    every profiled Llama shape, tables/b200_decode.medians.json)."""
+    table = None
+    for name in ("b200_decode.tbl", "b200_llama2_7b.tbl"):
+        path = os.path.join(ROOT, "tables", name)
+        if os.path.exists(path):
+            table = D.load_table(path)
+            break
+    if table is None:
+        table = D.DispatchTable(fingerprint=D.default_fingerprint())
+    for n, k in cfg.gemm_shapes(tp).values():
+        if (n, k) not in table.entries:
+            table.add(D.DispatchEntry(n=n, k=k, m1=1, m2=128))
+    return table
+
+
+def _rotating_graph_time(torch, fns, reps=5):
+    """Device seconds per call of a list of launch closures (one CUDA graph
+    holding them all, replayed reps times): operands rotate so the working set
+    exceeds L2."""
+    t = _op_graph_time(torch, lambda: [f() for f in fns], reps)
+    return t / len(fns)
+
+
+def config1_attention_op(torch, fd, peak):
+    """configs[0]: async decode attention op alone, B=1, 32 heads x 128, L=1024,
+    fp16, N(0,1) inputs, golden calibration; in-graph over 8 rotating caches."""
+    B, H, L, Dh = 1, 32, 1024, 128
+    g = torch.Generator(device="cuda").manual_seed(0)
+    cal = fd.ScalingCalibration(phi=-7.775933742523193, a=-1.0, b=16.577659606933594, coverage=1.0)
+    cfg = fd.AttentionConfig(p=0, scale=1 / math.sqrt(Dh), calib=cal)
+    q = torch.randn((B, H, Dh), generator=g, device="cuda").half()
+    out = torch.empty_like(q)
+    kvs = [(torch.randn((B, H, L, Dh), generator=g, device="cuda").half(),
+            torch.randn((B, H, L, Dh), generator=g, device="cuda").half()) for _ in range(8)]
+    fns = [lambda k=k, v=v: fd.decode_attention(q, k, v, cfg, "async", out=out) for k, v in kvs]
+    t = _rotating_graph_time(torch, fns)
+    byt = 2 * B * H * L * Dh * 2 + 2 * B * H * Dh * 2
+    return {"us": round(t * 1e6, 2), "bytes": byt, "gbs": round(byt / t / 1e9, 1),
+            "frac": round(byt / t / 1e9 / peak, 3), "plan": list(fd.attention.plan(q, kvs[0][0], cfg)),
+            "launches_per_call": 2, "note": "2 launches (async + recompute check); 16.8 MB moves in "
+            "~2.6 us at HBM speed, so launch/ramp latency dominates at this size"}
+
+
+def config2_gemm_sweep(torch, fd, D, table, peak):
+    """configs[1]: flat GEMM + dispatch over M in {1..64} x the Llama-2-7B
+    projection shapes; in-graph, rotating weights (> L2)."""
+    res = {}
+    for n, k in ((12288, 4096), (4096, 4096), (11008, 4096), (4096, 11008)):
+        nrot = max(4, min(16, int(1.2e9 // (n * k * 2))))
+        ws = [fd.PackedWeight((torch.randn((n, k), device="cuda") / k ** 0.5).half(), k, n)
+              for _ in range(nrot)]
+        row = {}
+        for m in (1, 2, 4, 8, 16, 32, 64):
+            a = torch.randn((m, k), device="cuda").half()
+            out = torch.empty((m, n), device="cuda", dtype=torch.half)
+            ch = D.dispatch(m, n, k, table)
+            t = _rotating_graph_time(torch, [lambda w=w: D.run_device(ch, a, w, out=out) for w in ws])
+            byt = n * k * 2 + m * k * 2 + m * n * 2
+            row[str(m)] = {"choice": ch.value, "us": round(t * 1e6, 2), "gbs": round(byt / t / 1e9, 1),
+                           "frac": round(byt / t / 1e9 / peak, 3)}
+        res[f"{n}x{k}"] = row
+        del ws
+    return res
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -175,21 +250,40 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
+    import paper_2311_01282_b200 as fd
     from paper_2311_01282_b200 import llama
     from paper_2311_01282_b200.attention import decode_attention
     import importlib
     D = importlib.import_module("paper_2311_01282_b200.dispatch")
 
-    cfg = llama.LLAMA2_7B
+    cfg = getattr(llama, MODELS[args.model])
+    # tensor parallelism: --tp T over the launched ranks (dp = world / T groups);
+    # --tp-shard T on one process: rank 0's shard alone, all-reduce omitted
+    tp = args.tp if args.tp > 1 else 1
+    shard_only = args.tp_shard > 1 and world == 1
+    if shard_only:
+        tp = args.tp_shard
+    if world % (1 if shard_only else tp):
+        raise SystemExit(f"--tp {tp} must divide the world size {world}")
+    dp = world // (1 if shard_only else tp)
+    tp_rank = 0 if shard_only else rank % tp
+    group = None
+    if tp > 1 and not shard_only:
+        groups = [dist.new_group(list(range(d * tp, (d + 1) * tp))) for d in range(dp)]
+        group = groups[rank // tp]
     B, L, K, W = args.batch, args.kv_len, args.steps, args.warmup
-    table = None
-    tpath = os.path.join(ROOT, "tables", "b200_llama2_7b.tbl")
-    if os.path.exists(tpath):
-        table = D.load_table(tpath)
-        if any((n, k) not in table.entries for n, k in cfg.gemm_shapes().values()):
-            table = None
-    dec = llama.LlamaDecoder(cfg, B, L + K + W + 8, table=table, seed=1000 + rank)
-    dec.prefill_random(L, seed=2000 + rank)
+    table = _load_table(D, cfg, tp)
+    dec = llama.LlamaDecoder(cfg, B, L + K + W + 8, table=table, seed=1000 + rank // tp,
+                             tp_rank=tp_rank, tp_size=tp, group=group, collective=not shard_only)
+    dec.prefill_random(L, seed=2000 + rank // tp)
+    if args.inject:
+        # configs[3]: force the synchronized-softmax recompute: one key far
+        # outside the calibrated band in `inject` (batch, kv-head) groups of
+        # every layer flags all G query rows of those groups
+        for kc in dec.k_cache:
+            for r in range(args.inject):
+                b, h = r % B, (r // B) % dec.n_kv_heads_local
+                kc[b, h, L // 2].mul_(40.0)
     dec.capture()
     for _ in range(W):
         dec.step()
@@ -212,7 +306,7 @@ def run_gpu(args):
         t = torch.tensor([secs], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         secs = float(t.item())
-    value = world * B * K / secs
+    value = dp * B * K / secs          # tokens: each TP group decodes one batch
     ms_per_step = secs / K * 1e3
     recomputed = int(dec.recomputed.item())
 
@@ -237,12 +331,11 @@ def run_gpu(args):
         t = torch.tensor([e2e_secs], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_secs = float(t.item())
-    e2e_value = world * B * K / e2e_secs
+    e2e_value = dp * B * K / e2e_secs
 
     # ---- per-op device time over all layers (roofline of the dominant kernel)
     reps = 3
-    Lmid = L + W + K + K // 2     # attended length mid-way through the timed region
-    hq, dh, hkv = cfg.n_heads, cfg.head_dim, cfg.n_kv_heads
+    hq, dh, hkv = dec.n_heads_local, cfg.head_dim, dec.n_kv_heads_local
     ops = {}
 
     def attn_all():
@@ -255,14 +348,15 @@ def run_gpu(args):
     attn_bytes = B * hkv * Lnow * dh * 2 * 2 + 2 * B * hq * dh * 2
     ops["attention_async(+recompute)"] = {"s_per_launch": t_attn, "bytes": attn_bytes,
                                           "launches_per_step": dec.n_layers}
-    shapes = cfg.gemm_shapes()
+    shapes = cfg.gemm_shapes(tp)
     from paper_2311_01282_b200.gemm import run_fused
     gb = lambda n, k: n * k * 2 + B * k * 2 + B * n * 2  # noqa: E731
     if dec.fused:
         L0 = dec.layers
+        st = 1 if tp > 1 else dec.ssq_tiles
         per_op = {
             f"gemm_qkv+rmsnorm+rope[{shapes['qkv'][0]}x{shapes['qkv'][1]}]:ImplB": (
-                lambda: [run_fused(dec.x, Ld["qkv_f"], x_op=3, ssq_in=dec.ssq_a, ssq_tiles=dec.ssq_tiles,
+                lambda: [run_fused(dec.x, Ld["qkv_f"], x_op=3, ssq_in=dec.ssq_a, ssq_tiles=st,
                                    eps=cfg.eps, ws_tag="decode_gemm",
                                    rope={"q_out": dec.q, "k_cache": dec.k_cache[i],
                                          "v_cache": dec.v_cache[i], "pos": dec.pos,
@@ -270,20 +364,22 @@ def run_gpu(args):
                 gb(*shapes["qkv"]), len(L0)),
             f"gemm_o+residual+ssq[{shapes['o'][0]}x{shapes['o'][1]}]:ImplB": (
                 lambda: [run_fused(dec.attn.view(B, hq * dh), Ld["o"], out=dec.h, residual=dec.x,
-                                   ssq_out=dec.ssq_b, ws_tag="decode_gemm") for Ld in L0],
+                                   ssq_out=None if tp > 1 else dec.ssq_b, ws_tag="decode_gemm")
+                         for Ld in L0],
                 gb(*shapes["o"]), len(L0)),
             f"gemm_gate_up+rmsnorm[{shapes['gate_up'][0]}x{shapes['gate_up'][1]}]:ImplB": (
                 lambda: [run_fused(dec.x, Ld["gate_up_f"], out=dec.gu, x_op=3, ssq_in=dec.ssq_b,
-                                   ssq_tiles=dec.ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
+                                   ssq_tiles=st, eps=cfg.eps, ws_tag="decode_gemm")
                          for Ld in L0],
                 gb(*shapes["gate_up"]), len(L0)),
             f"gemm_down+residual+ssq[{shapes['down'][0]}x{shapes['down'][1]}]:ImplB": (
                 lambda: [run_fused(dec.act, Ld["down"], out=dec.h, residual=dec.x,
-                                   ssq_out=dec.ssq_a, ws_tag="decode_gemm") for Ld in L0],
+                                   ssq_out=None if tp > 1 else dec.ssq_a, ws_tag="decode_gemm")
+                         for Ld in L0],
                 gb(*shapes["down"]), len(L0)),
             f"gemm_lm_head+rmsnorm[{shapes['lm_head'][0]}x{shapes['lm_head'][1]}]:ImplB": (
                 lambda: run_fused(dec.x, dec.lm_head_f, out=dec.logits, x_op=3, ssq_in=dec.ssq_a,
-                                  ssq_tiles=dec.ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm"),
+                                  ssq_tiles=st, eps=cfg.eps, ws_tag="decode_gemm"),
                 gb(*shapes["lm_head"]), 1),
         }
     else:
@@ -311,22 +407,31 @@ def run_gpu(args):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom_name.split("[")[0].split(":")[0])
+            tr = json.load(open(tpath))
+            key = dom_name.split("[")[0].split(":")[0]
+            traffic = tr.get(f"{args.model}/B{B}/L{L}", {}).get(key)
         except Exception:
             traffic = None
-    step_bytes = cfg.weight_bytes() + B * Lnow * cfg.kv_bytes_per_token()
-
+    step_bytes = cfg.weight_bytes(tp=tp) + B * Lnow * cfg.kv_bytes_per_token(tp=tp)
+    default_run = args.model == "llama2-7b" and tp == 1
+    workload = {"llama2-7b": "llama2-7b decode step (configs[2])",
+                "chatglm2-6b": "chatglm2-6b MQA decode step (configs[3])",
+                "llama2-70b": "llama2-70b GQA decode step (configs[4])"}[args.model]
+    par = f"dp{dp}" + (f"xtp{tp}" if tp > 1 and not shard_only else "")
+    if shard_only:
+        par = f"one tp{tp} shard on 1 GPU (all-reduce omitted)"
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-        "config": {"workload": "llama2-7b decode step (configs[2])", "model": "Llama-2-7B geometry, random-init",
-                   "layer": "real Llama (gate GEMM, RMSNorm, RoPE, residual, LM head)",
-                   "global_batch": world * B, "batch_per_gpu": B, "kv_len": L,
-                   "parallelism": f"dp{world} (replicas, no collective)",
-                   "l2": "inputs larger than L2 (13.2 GB weights + KV per step)",
-                   "attention": f"async unified-phi, p={dec.attn_cfg.p or 'auto'}",
-                   "gemm_choices": {op: c.value for op, c in dec.choices.items()}},
+        "config": {"workload": workload, "model": f"{cfg.name} geometry, random-init",
+                   "layer": "Llama-style layer (gate GEMM, RMSNorm, RoPE, residual, LM head)",
+                   "global_batch": dp * B, "batch_per_gpu": B, "kv_len": L, "parallelism": par,
+                   "l2": f"inputs larger than L2 ({cfg.weight_bytes(tp=tp) / 1e9:.1f} GB weights + KV per step)",
+                   "attention": f"async unified-phi, p={dec.attn_cfg.p or 'auto'}"
+                                + (", GQA/MQA on tensor cores" if cfg.n_heads // cfg.n_kv_heads >= 4 else ""),
+                   "gemm_choices": {op: c.value for op, c in dec.choices.items()},
+                   "injected_groups_per_layer": args.inject},
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": B * 4,
                 "d2h_bytes_per_step": B * 4},
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(dom["gbs"], 1),
@@ -343,6 +448,9 @@ def run_gpu(args):
         "rows_recomputed": recomputed,
         "clocks": clk.summary(),
     }
+    if rank == 0 and world == 1 and default_run and not args.no_extras:
+        line["configs"] = {"c1_attention_op_b1_l1024": config1_attention_op(torch, fd, peak),
+                           "c2_gemm_dispatch_sweep": config2_gemm_sweep(torch, fd, D, table, peak)}
     if rank == 0 and world == 1 and not args.no_cpu:
         t_step, desc, cores = cpu_reference_step(B, L, cfg)
         line["cpu_baseline"] = {"value": round(B / t_step, 4), "unit": UNIT, "cores": cores,
@@ -360,12 +468,14 @@ def run_reference(args):
     if rank != 0:
         return
     from paper_2311_01282_b200 import llama  # config only (no GPU work)
-    cfg = llama.LLAMA2_7B
+    cfg = getattr(llama, MODELS[args.model])
     B, L = args.batch, args.kv_len
     steps = []
     desc, cores = "", 0
+    # each step is a bounded sample (~1 s on a 16-core host): 1/16 of every
+    # projection's columns + 4 attention heads, scaled to the full step
     for i in range(args.warmup + args.steps):
-        t, desc, cores = cpu_reference_step(B, L, cfg, rng_seed=i)
+        t, desc, cores = cpu_reference_step(B, L, cfg, rng_seed=i, head_sample=4, n_frac=16)
         if i >= args.warmup:
             steps.append(t)
     import numpy as np
@@ -375,7 +485,7 @@ def run_reference(args):
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-        "config": {"workload": "llama2-7b decode step (configs[2])", "model": "Llama-2-7B geometry, random-init",
+        "config": {"workload": f"{args.model} decode step", "model": f"{cfg.name} geometry, random-init",
                    "global_batch": B, "batch_per_gpu": B, "kv_len": L,
                    "parallelism": "host CPU (reference numba path, restated in C)"},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
@@ -388,12 +498,19 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--kv-len", type=int, default=1024)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extras", action="store_true", help="skip the configs[0]/[1] sub-benchmarks")
+    ap.add_argument("--model", default="llama2-7b", choices=sorted(MODELS))
+    ap.add_argument("--tp", type=int, default=1, help="tensor-parallel ranks per replica (torchrun)")
+    ap.add_argument("--tp-shard", type=int, default=1,
+                    help="single GPU: run rank 0's shard of a T-way TP step (all-reduce omitted)")
+    ap.add_argument("--inject", type=int, default=0,
+                    help="(batch, kv-head) groups per layer forced through the recompute path")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

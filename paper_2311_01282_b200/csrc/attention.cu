@@ -767,10 +767,11 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
         FDPP_REQUIRE(p->p <= ATT_MAX_P, FDPP_ERR_VALUE, "partition count above %d", ATT_MAX_P);
         lay->p = p->p;
     } else if (lay->mma) {
-        // auto, tensor-core path: ~2 CTAs per SM in one wave, >= 512 keys each
-        // (fewer, longer CTAs amortise the per-CTA ramp: profiles/r1_attn_gqa_sweep.txt)
-        int want = (2 * sms + launch_groups - 1) / launch_groups;
-        int maxp = p->L / 512 > 0 ? p->L / 512 : 1;
+        // auto, tensor-core path: one full wave (3 CTAs per SM: each CTA keeps
+        // 64 KB of K/V in flight, so the whole wave is what saturates HBM), no
+        // second partial wave, >= 128 keys per CTA (profiles/r1_attn_gqa_sweep.txt)
+        int want = (3 * sms) / launch_groups;
+        int maxp = p->L / 128 > 0 ? p->L / 128 : 1;
         lay->p = want < 1 ? 1 : (want > maxp ? maxp : want);
         if (lay->p > ATT_MAX_P) lay->p = ATT_MAX_P;
     } else {

@@ -101,7 +101,8 @@ class LlamaDecoder:
     def __init__(self, cfg: LlamaConfig, batch: int, max_len: int, *, table=None,
                  calib: ScalingCalibration = GOLDEN_CALIB, dtype=torch.float16, seed: int = 0,
                  attn_p: int = 0, attn_splits: int = 0, n_layers: int = None, fused: bool = True,
-                 tp_rank: int = 0, tp_size: int = 1, group=None, weights: dict = None):
+                 tp_rank: int = 0, tp_size: int = 1, group=None, weights: dict = None,
+                 collective: bool = True):
         """tp_size > 1: this process is rank tp_rank of a tensor-parallel group
         (tp.py): sharded QKV / O / gate|up / down, local heads and KV cache, one
         NCCL all-reduce of the residual stream after O and after down (captured
@@ -112,6 +113,9 @@ class LlamaDecoder:
         self.cfg, self.B, self.max_len, self.dtype = cfg, batch, max_len, dtype
         self.n_layers = n_layers or cfg.n_layers
         self.tp_rank, self.tp_size, self.group = tp_rank, tp_size, group
+        # collective=False: one rank's shard alone on one GPU (per-GPU compute of a
+        # t-way TP step; the all-reduce is omitted, the row-ssq kernel still runs)
+        self.collective = collective
         sd = _tp.shard_dims(cfg, tp_size)
         dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
@@ -242,7 +246,8 @@ class LlamaDecoder:
             # x = sum over ranks of (x + partial_0, partial_1, ...); then the
             # next projection's folded-RMSNorm input (one tile per row)
             import torch.distributed as dist
-            dist.all_reduce(self.x, group=self.group)
+            if self.collective:
+                dist.all_reduce(self.x, group=self.group)
             _lib.check(lib.fdpp_row_ssq(self.x.data_ptr(), ssq.data_ptr(), B, cfg.hidden, dt,
                                         _lib.stream_handle()), "row_ssq")
 

@@ -10,11 +10,13 @@ import paper_2311_01282_b200  # noqa: E402,F401
 from paper_2311_01282_b200 import llama  # noqa: E402
 
 D = importlib.import_module("paper_2311_01282_b200.dispatch")
-out = sys.argv[1] if len(sys.argv) > 1 else "tables/b200_llama2_7b.tbl"
-cfgs = [llama.LLAMA2_7B] + ([llama.LLAMA2_70B] if "--70b" in sys.argv else [])
+out = sys.argv[1] if len(sys.argv) > 1 else "tables/b200_decode.tbl"
+# every decode-step GEMM shape the bench can run: Llama-2-7B, ChatGLM2-6B, and
+# Llama-2-70B per rank at t = 1/2/4/8, plus config 2's shapes
+runs = [(llama.LLAMA2_7B, 1), (llama.CHATGLM2_6B, 1)] + [(llama.LLAMA2_70B, t) for t in (1, 2, 4, 8)]
 table = D.DispatchTable(fingerprint=D.default_fingerprint())
 details = {}
-shapes = sorted({s for c in cfgs for s in c.gemm_shapes().values()} |
+shapes = sorted({s for c, t in runs for s in c.gemm_shapes(t).values()} |
                 {(12288, 4096), (4096, 4096), (11008, 4096), (4096, 11008)})
 for n, k in shapes:
     det = []
