@@ -53,6 +53,12 @@ struct AttnArgs {
     float *ws_m;    // [B*Hq][p*nsub]
     int *ws_viol;   // [B*Hq][p*nsub]
     int *counters;  // [B*Hkv*n_rg]
+    // flagged (batch, kv-head) list: the async join appends, the recompute
+    // launch walks it (list_mode) instead of one CTA per row group
+    int *flag_list;   // [B*Hkv]
+    int *flag_mark;   // [B*Hkv] dedupe markers
+    int *flag_count;  // [0] entries, [32] CTAs done (reset by the recompute launch)
+    bool list_mode;
 };
 
 template <typename T, int D>
@@ -139,10 +145,16 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 // 16-key slice S = Q K^T, the unified-phi band check and e^(x - phi) in fp32
 // (exp-sums stay fp32), P = e * pscale packed to 16 bits as the next MMA's A
 // operand straight from the accumulators, O += P V.
-template <typename T, int D, int GT, bool ASYNC, bool MMA = false>
-__global__ void __launch_bounds__(ATT_THREADS, MMA ? 3 : 1)  // MMA: 3 CTAs / SM (192 KB of ring in flight)
-attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
-                  const __grid_constant__ CUtensorMap tmV) {
+// append (batch, kv-head) to the recompute list once per launch
+__device__ __forceinline__ void flag_group(const AttnArgs &a, int b, int kvh) {
+    if (!a.flag_list) return;
+    const int e = b * a.Hkv + kvh;
+    if (atomicExch(&a.flag_mark[e], 1) == 0) a.flag_list[atomicAdd(a.flag_count, 1)] = e;
+}
+
+template <typename T, int D, int GT, bool ASYNC, bool MMA>
+__device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap &tmK, const CUtensorMap &tmV,
+                                         const int cta, const int by, const int b) {
     using Gm = AttnGeom<T, D>;
     constexpr int VEC = Gm::VEC, LPK = Gm::LPK, KPI = Gm::KPI, TK = Gm::TK, RB = Gm::RB;
     constexpr int NRED = MMA ? 1 : ATT_CONSUMERS;  // per-warp partial buffers in `red`
@@ -161,13 +173,13 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
     int *s_cviol = reinterpret_cast<int *>(smem) + ATT_MAX_P;
     int *s_unrep = reinterpret_cast<int *>(smem) + 2 * ATT_MAX_P;
     static_assert(ATT_STAGES * Gm::STAGE_BYTES >= 3 * ATT_MAX_P * 4, "join scratch");
-    __shared__ int s_last, s_any_flag;
+    __shared__ int s_last, s_any_flag, s_grp_flag;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int P = args.p * args.nsub;
-    const int cta = blockIdx.x;               // (chunk, sub) index in [0, P)
+    // cta: (chunk, sub) index in [0, P); by: kv-head x row group; b: batch row
     const int j = cta / args.nsub, sub = cta % args.nsub;
-    const int rg = blockIdx.y % args.n_rg, kvh = blockIdx.y / args.n_rg, b = blockIdx.z;
+    const int rg = by % args.n_rg, kvh = by / args.n_rg;
     const int g0 = rg * GT;
     const int gcount = min(GT, args.G - g0);
     const int h0 = kvh * args.G + g0;         // first query head of this row group
@@ -511,6 +523,10 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    if (ASYNC) {
+        if (threadIdx.x == 0) s_grp_flag = 0;
+        __syncthreads();
+    }
 
     if (ASYNC && !args.viol_index && !args.chunk_num && !args.chunk_den) {
         // decode hot path (no per-chunk outputs requested): one warp per query
@@ -569,7 +585,10 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
             for (int o = 16; o > 0; o >>= 1) dpart += __shfl_xor_sync(0xffffffffu, dpart, o);
             if (lane == 0) {
                 args.row_flags[row] = flagged ? 1 : 0;
-                if (flagged && args.rows_recomputed) atomicAdd(args.rows_recomputed, 1);
+                if (flagged) {
+                    if (args.rows_recomputed) atomicAdd(args.rows_recomputed, 1);
+                    s_grp_flag = 1;
+                }
             }
             if (!flagged) {
                 T *op = static_cast<T *>(args.o) + (int64_t)b * args.o_sb + (int64_t)(h0 + g) * args.o_sh;
@@ -578,6 +597,8 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
                     if (lane + 32 * r < D) op[lane + 32 * r] = Elem<T>::from_f(acc[r] / dpart);
             }
         }
+        __syncthreads();
+        if (threadIdx.x == 0 && s_grp_flag) flag_group(args, b, kvh);
         return;
     }
     constexpr int LB = 32;  // partial loads kept in flight per thread
@@ -659,6 +680,7 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
             if (threadIdx.x == 0) {
                 args.row_flags[row] = flagged ? 1 : 0;
                 if (flagged && args.rows_recomputed) atomicAdd(args.rows_recomputed, 1);
+                if (flagged) s_grp_flag = 1;
             }
             if (!flagged) {
                 float dsum = 0.f;
@@ -705,6 +727,48 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
             __syncthreads();
         }
     }
+    if (ASYNC && threadIdx.x == 0 && s_grp_flag) flag_group(args, b, kvh);
+}
+
+// One CTA per (chunk/sub-range, kv-head x row group, batch row); the recompute
+// launch (list_mode) instead walks the (batch, kv-head) groups the async join
+// flagged, with a small fixed grid: a clean step costs one near-empty wave
+// instead of B x Hkv x n_rg x P early-exit CTAs.
+template <typename T, int D, int GT, bool ASYNC, bool MMA = false>
+__global__ void __launch_bounds__(ATT_THREADS, MMA ? 3 : 1)  // MMA: 3 CTAs / SM (192 KB of ring in flight)
+attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
+                  const __grid_constant__ CUtensorMap tmV) {
+    if constexpr (!ASYNC) {
+        if (args.list_mode) {
+            pdl_wait();  // the list comes from the async launch
+            const int count = __ldcg(args.flag_count);
+            const int P = args.p * args.nsub;
+            const int64_t items = (int64_t)count * args.n_rg * P;
+            for (int64_t i = blockIdx.x; i < items; i += gridDim.x) {
+                const int x = (int)(i % P);
+                const int64_t r = i / P;
+                const int rg = (int)(r % args.n_rg);
+                const int e = __ldcg(&args.flag_list[r / args.n_rg]);  // b * Hkv + kvh
+                const int b = e / args.Hkv, kvh = e % args.Hkv;
+                attn_cta<T, D, GT, ASYNC, MMA>(args, tmK, tmV, x, kvh * args.n_rg + rg, b);
+                __syncthreads();  // shared memory is reused by the next item
+            }
+            pdl_trigger();
+            // the last CTA clears the list and its dedupe markers (graph replay)
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                if (atomicAdd(&args.flag_count[32], 1) == (int)gridDim.x - 1) {
+                    __threadfence();
+                    for (int k = 0; k < count; ++k) args.flag_mark[__ldcg(&args.flag_list[k])] = 0;
+                    args.flag_count[0] = 0;
+                    args.flag_count[32] = 0;
+                }
+            }
+            return;
+        }
+    }
+    attn_cta<T, D, GT, ASYNC, MMA>(args, tmK, tmV, blockIdx.x, blockIdx.y, blockIdx.z);
 }
 
 // ---------------------------------------------------------------------- host
@@ -713,8 +777,13 @@ struct AttnLayout {
     bool mma;      // async launch on tensor cores (GQA/MQA): 16-row groups
     int n_rg_mma;  // its row groups per kv head
     float pscale;  // its power-of-two P scale
-    size_t off_num, off_den, off_m, off_viol, off_cnt, total;
+    size_t off_num, off_den, off_m, off_viol, off_cnt, off_flags, total;
 };
+
+// recompute list header (fixed offset after the ticket counters, never aliased,
+// left zeroed by every launch): [0] count, [32] CTAs done, list, dedupe marks
+constexpr int kFlagListOff = 64, kFlagMax = 8128;
+constexpr size_t kFlagBytes = 16384 * sizeof(int);
 
 static int pick_gt(int G) { return G >= 8 ? 8 : G >= 4 ? 4 : G >= 2 ? 2 : 1; }
 
@@ -799,6 +868,7 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
     size_t off = 0;
     FDPP_REQUIRE(groups <= kWsCounters, FDPP_ERR_SHAPE, "too many (batch, kv-head) groups: %d", groups);
     lay->off_cnt = off;  off += kWsCounterBytes;
+    lay->off_flags = off; off += kFlagBytes;
     lay->off_num = off;  off += al(rows * lay->P * p->D * sizeof(float));
     lay->off_den = off;  off += al(rows * lay->P * sizeof(float));
     lay->off_m = off;    off += al(rows * lay->P * sizeof(float));
@@ -822,7 +892,8 @@ static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st,
         if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn)");
         attr = true;
     }
-    dim3 grid(grid_x, a.Hkv * a.n_rg, a.B);
+    // list_mode: grid_x CTAs walk the flagged-group list
+    dim3 grid = a.list_mode ? dim3(grid_x) : dim3(grid_x, a.Hkv * a.n_rg, a.B);
     cudaError_t e = launch_kernel(kern, grid, dim3(ATT_THREADS), smem, st, a, tmK ? *tmK : none,
                                   tmV ? *tmV : none);
     if (e != cudaSuccess) return cuda_status(e, "attn_split_kernel launch");
@@ -935,6 +1006,12 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     a.ws_m = reinterpret_cast<float *>(ws + lay.off_m);
     a.ws_viol = reinterpret_cast<int *>(ws + lay.off_viol);
     a.counters = reinterpret_cast<int *>(ws + lay.off_cnt);
+    const bool use_list = (int64_t)p->B * p->Hkv <= kFlagMax;
+    int *flags = reinterpret_cast<int *>(ws + lay.off_flags);
+    a.flag_count = flags;
+    a.flag_list = use_list ? flags + kFlagListOff : nullptr;
+    a.flag_mark = flags + kFlagListOff + kFlagMax;
+    a.list_mode = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (p->mode == FDPP_ATTN_SYNC) {
         a.only_flagged = false;
@@ -959,5 +1036,10 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     if (s != FDPP_OK) return s;
     // synchronized recompute of flagged rows (attention.py:283-285), always launched
     a.only_flagged = true;
+    if (use_list) {  // walk the flagged (batch, kv-head) list with one small wave
+        const int sms = sm_count() > 0 ? sm_count() : 148;
+        a.list_mode = true;
+        return by_dtype<false>(a, p->dtype, p->D, lay.GT, 2 * sms, st);
+    }
     return by_dtype<false>(a, p->dtype, p->D, lay.GT, lay.P, st);
 }
