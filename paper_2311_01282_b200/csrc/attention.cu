@@ -157,8 +157,9 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                                          const int cta, const int by, const int b) {
     using Gm = AttnGeom<T, D>;
     constexpr int VEC = Gm::VEC, LPK = Gm::LPK, KPI = Gm::KPI, TK = Gm::TK, RB = Gm::RB;
-    constexpr int NRED = MMA ? 1 : ATT_CONSUMERS;  // per-warp partial buffers in `red`
-    static_assert(!MMA || (ASYNC && GT == 16 && D == 128 && sizeof(T) == 2 && TK % 32 == 0), "MMA path");
+    // per-warp partial buffers in `red` (the async MMA path accumulates warps in place)
+    constexpr int NRED = (MMA && ASYNC) ? 1 : ATT_CONSUMERS;
+    static_assert(!MMA || (GT == 16 && D == 128 && sizeof(T) == 2 && TK % 32 == 0), "MMA path");
 
     extern __shared__ __align__(128) uint8_t smem_raw[];
     // the MMA path's TMA swizzle needs 1024-byte aligned stages
@@ -264,6 +265,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
         for (int nb = 0; nb < D / 8; ++nb) o[nb][0] = o[nb][1] = o[nb][2] = o[nb][3] = 0.f;
         float den0 = 0.f, den1 = 0.f;
         int viol0 = INT_MAX, viol1 = INT_MAX;
+        float mx0 = -INFINITY, mx1 = -INFINITY;  // sync: running row maxima
         const float scale = args.scale, phi = args.phi, ba = args.a, bb = args.b, ps = args.pscale;
         const int mi = lane >> 3, mr = lane & 7;  // ldmatrix: matrix / row this lane addresses
         for (int t = warp >> 1; t < ntiles; t += 2) {
@@ -287,24 +289,67 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                         mma_16816<T>(sacc[1], qa[kk], kb[2], kb[3]);
                     }
                 }
-                // unified phi: band check, e^(x - phi) in fp32, P = e * pscale (16-bit)
                 float ep[2][4];
+                if constexpr (ASYNC) {
+                    // unified phi: band check, e^(x - phi) in fp32, P = e * pscale (16-bit)
 #pragma unroll
-                for (int nb = 0; nb < 2; ++nb)
+                    for (int nb = 0; nb < 2; ++nb)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int key = k0 + 8 * nb + cq + (i & 1);
-                        const float ti = sacc[nb][i] * scale - phi;
-                        const bool valid = key < n, bad = (ti <= ba) || (ti >= bb);
-                        if (valid && bad) {
-                            if (i < 2) viol0 = min(viol0, key0 + key);
-                            else viol1 = min(viol1, key0 + key);
+                        for (int i = 0; i < 4; ++i) {
+                            const int key = k0 + 8 * nb + cq + (i & 1);
+                            const float ti = sacc[nb][i] * scale - phi;
+                            const bool valid = key < n, bad = (ti <= ba) || (ti >= bb);
+                            if (valid && bad) {
+                                if (i < 2) viol0 = min(viol0, key0 + key);
+                                else viol1 = min(viol1, key0 + key);
+                            }
+                            const float e = (valid && !bad) ? __expf(ti) : 0.f;
+                            if (i < 2) den0 += e;
+                            else den1 += e;
+                            ep[nb][i] = e * ps;
                         }
-                        const float e = (valid && !bad) ? __expf(ti) : 0.f;
-                        if (i < 2) den0 += e;
-                        else den1 += e;
-                        ep[nb][i] = e * ps;
+                } else {
+                    // synchronized softmax (FlashDecoding, attention.py:91-162): per-row
+                    // running max over the slice (quad-shared rows), rescale, P <= 1
+                    float sm0 = -INFINITY, sm1 = -INFINITY;
+#pragma unroll
+                    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int key = k0 + 8 * nb + cq + (i & 1);
+                            sacc[nb][i] = key < n ? sacc[nb][i] * scale : -INFINITY;
+                            if (i < 2) sm0 = fmaxf(sm0, sacc[nb][i]);
+                            else sm1 = fmaxf(sm1, sacc[nb][i]);
+                        }
+#pragma unroll
+                    for (int off = 1; off < 4; off <<= 1) {
+                        sm0 = fmaxf(sm0, __shfl_xor_sync(0xffffffffu, sm0, off));
+                        sm1 = fmaxf(sm1, __shfl_xor_sync(0xffffffffu, sm1, off));
                     }
+                    const float n0 = fmaxf(mx0, sm0), n1 = fmaxf(mx1, sm1);
+                    const float f0 = safe_scale(mx0, n0), f1 = safe_scale(mx1, n1);
+                    mx0 = n0;
+                    mx1 = n1;
+                    den0 *= f0;
+                    den1 *= f1;
+#pragma unroll
+                    for (int nb2 = 0; nb2 < D / 8; ++nb2) {
+                        o[nb2][0] *= f0;
+                        o[nb2][1] *= f0;
+                        o[nb2][2] *= f1;
+                        o[nb2][3] *= f1;
+                    }
+#pragma unroll
+                    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float m = i < 2 ? mx0 : mx1;
+                            const float e = m == -INFINITY ? 0.f : __expf(sacc[nb][i] - m);
+                            if (i < 2) den0 += e;
+                            else den1 += e;
+                            ep[nb][i] = e;
+                        }
+                }
                 const uint32_t pa[4] = {pack2<T>(ep[0][0], ep[0][1]), pack2<T>(ep[0][2], ep[0][3]),
                                         pack2<T>(ep[1][0], ep[1][1]), pack2<T>(ep[1][2], ep[1][3])};
                 // O += P V
@@ -323,7 +368,8 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
-        // rows r0 / r0+8 are shared by the lane quad: fixed butterfly
+        // rows r0 / r0+8 are shared by the lane quad: fixed butterfly (sync: the
+        // quad already shares one running max per row)
 #pragma unroll
         for (int off = 1; off < 4; off <<= 1) {
             den0 += __shfl_xor_sync(0xffffffffu, den0, off);
@@ -332,6 +378,21 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
             viol1 = min(viol1, __shfl_xor_sync(0xffffffffu, viol1, off));
         }
         pdl_trigger();  // main stream done: the next kernel may start its prologue
+        if constexpr (!ASYNC) {
+            // per-warp partials (num, den, running max) for the Eq. (2) merge below
+            float *rw = red + warp * GT * (D + 2);
+#pragma unroll
+            for (int nb = 0; nb < D / 8; ++nb)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    rw[(r0 + (i >> 1) * 8) * (D + 2) + 8 * nb + cq + (i & 1)] = o[nb][i];
+            if ((lane & 3) == 0) {
+                rw[r0 * (D + 2) + D] = den0;
+                rw[(r0 + 8) * (D + 2) + D] = den1;
+                rw[r0 * (D + 2) + D + 1] = mx0;
+                rw[(r0 + 8) * (D + 2) + D + 1] = mx1;
+            }
+        } else {
         // warps add into one [GT][D+2] buffer in fixed order (numerators unscaled exactly)
         const float ips = args.inv_pscale;
 #pragma unroll 1
@@ -354,6 +415,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
             }
             named_bar_sync(1, ATT_CONSUMERS * 32);
         }
+        }  // ASYNC
     } else {
         // ------------------------------------------------ consumer warps
         const int c = lane % LPK;          // 16-B chunk of the head dim owned by this lane
@@ -800,12 +862,15 @@ static bool mma_enabled() {
     return v != 0;
 }
 
-static bool mma_eligible(const fdpp_attn_params *p, int G, float *pscale) {
-    if (!mma_enabled() || p->mode != FDPP_ATTN_ASYNC || G < 4 || p->D != 128) return false;
+static bool mma_shape_ok(const fdpp_attn_params *p, int G) {
+    if (!mma_enabled() || G < 4 || p->D != 128) return false;
     if (p->dtype != FDPP_F16 && p->dtype != FDPP_BF16) return false;
-    if (p->kv_stride_h % p->D != 0 || p->kv_stride_b != (int64_t)p->Hkv * p->kv_stride_h ||
-        p->kv_stride_h < (int64_t)p->L * p->D)
-        return false;
+    return p->kv_stride_h % p->D == 0 && p->kv_stride_b == (int64_t)p->Hkv * p->kv_stride_h &&
+           p->kv_stride_h >= (int64_t)p->L * p->D;
+}
+
+static bool mma_eligible(const fdpp_attn_params *p, int G, float *pscale) {
+    if (p->mode != FDPP_ATTN_ASYNC || !mma_shape_ok(p, G)) return false;
     const double log2e = 1.4426950408889634;
     if (p->dtype == FDPP_F16) {
         if (!(p->b > p->a) || (double)(p->b - p->a) * log2e > 28.0) return false;
@@ -882,7 +947,7 @@ static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st,
                                const CUtensorMap *tmK = nullptr, const CUtensorMap *tmV = nullptr) {
     using Gm = AttnGeom<T, D>;
     const int smem = (MMA ? 1024 : 0) + ATT_STAGES * Gm::STAGE_BYTES + 2 * ATT_STAGES * 8 +
-                     (MMA ? 1 : ATT_CONSUMERS) * GT * (D + 2) * (int)sizeof(float);
+                     ((MMA && ASYNC) ? 1 : ATT_CONSUMERS) * GT * (D + 2) * (int)sizeof(float);
     auto kern = attn_split_kernel<T, D, GT, ASYNC, MMA>;
     CUtensorMap none;
     memset(&none, 0, sizeof(none));
@@ -930,10 +995,19 @@ static fdpp_status by_d(const AttnArgs &a, int D, int gt, int gx, cudaStream_t s
     return FDPP_ERR_UNSUPPORTED;
 }
 
+template <bool ASYNC>
 static fdpp_status launch_mma(const AttnArgs &a, int dtype, int gx, const CUtensorMap *tmK,
                               const CUtensorMap *tmV, cudaStream_t st) {
-    return dtype == FDPP_BF16 ? launch_attn<__nv_bfloat16, 128, 16, true, true>(a, gx, st, tmK, tmV)
-                              : launch_attn<__half, 128, 16, true, true>(a, gx, st, tmK, tmV);
+    return dtype == FDPP_BF16 ? launch_attn<__nv_bfloat16, 128, 16, ASYNC, true>(a, gx, st, tmK, tmV)
+                              : launch_attn<__half, 128, 16, ASYNC, true>(a, gx, st, tmK, tmV);
+}
+
+// 2-D maps over the cache as [B * Hkv * Lmax rows, D]: 32-row x 64-column boxes
+static fdpp_status kv_maps(const fdpp_attn_params *p, CUtensorMap *mk, CUtensorMap *mv) {
+    const int64_t rows = (int64_t)p->B * p->Hkv * (p->kv_stride_h / p->D);
+    fdpp_status s = make_kmajor_map(mk, p->k, rows, p->D, p->D, 32, p->dtype);
+    if (s != FDPP_OK) return s;
+    return make_kmajor_map(mv, p->v, rows, p->D, p->D, 32, p->dtype);
 }
 
 template <bool ASYNC>
@@ -1013,23 +1087,28 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     a.flag_mark = flags + kFlagListOff + kFlagMax;
     a.list_mode = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    a.kv_rows_per_head = p->kv_stride_h / p->D;
+    const bool sync_mma = mma_shape_ok(p, lay.G);  // GQA/MQA sync softmax on tensor cores
+    CUtensorMap mk, mv;
+    if (sync_mma || lay.mma) {
+        if ((s = kv_maps(p, &mk, &mv)) != FDPP_OK) return s;
+    }
     if (p->mode == FDPP_ATTN_SYNC) {
         a.only_flagged = false;
+        if (sync_mma) {
+            AttnArgs am = a;
+            am.n_rg = lay.n_rg_mma;
+            return launch_mma<false>(am, p->dtype, lay.P, &mk, &mv, st);
+        }
         return by_dtype<false>(a, p->dtype, p->D, lay.GT, lay.P, st);
     }
     a.only_flagged = false;
     if (lay.mma) {
-        // 2-D maps over the cache as [B * Hkv * Lmax rows, D]: 32-row x 64-column boxes
-        CUtensorMap mk, mv;
-        const int64_t rows = (int64_t)p->B * p->Hkv * (p->kv_stride_h / p->D);
-        if ((s = make_kmajor_map(&mk, p->k, rows, p->D, p->D, 32, p->dtype)) != FDPP_OK) return s;
-        if ((s = make_kmajor_map(&mv, p->v, rows, p->D, p->D, 32, p->dtype)) != FDPP_OK) return s;
         AttnArgs am = a;
         am.n_rg = lay.n_rg_mma;
         am.pscale = lay.pscale;
         am.inv_pscale = 1.f / lay.pscale;
-        am.kv_rows_per_head = p->kv_stride_h / p->D;
-        s = launch_mma(am, p->dtype, lay.P, &mk, &mv, st);
+        s = launch_mma<true>(am, p->dtype, lay.P, &mk, &mv, st);
     } else {
         s = by_dtype<true>(a, p->dtype, p->D, lay.GT, lay.P, st);
     }
@@ -1039,6 +1118,11 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     if (use_list) {  // walk the flagged (batch, kv-head) list with one small wave
         const int sms = sm_count() > 0 ? sm_count() : 148;
         a.list_mode = true;
+        if (sync_mma) {
+            AttnArgs am = a;
+            am.n_rg = lay.n_rg_mma;
+            return launch_mma<false>(am, p->dtype, 2 * sms, &mk, &mv, st);
+        }
         return by_dtype<false>(a, p->dtype, p->D, lay.GT, 2 * sms, st);
     }
     return by_dtype<false>(a, p->dtype, p->D, lay.GT, lay.P, st);
