@@ -367,8 +367,8 @@ def run_gpu(args):
                                    ssq_out=None if tp > 1 else dec.ssq_b, ws_tag="decode_gemm")
                          for Ld in L0],
                 gb(*shapes["o"]), len(L0)),
-            f"gemm_gate_up+rmsnorm[{shapes['gate_up'][0]}x{shapes['gate_up'][1]}]:ImplB": (
-                lambda: [run_fused(dec.x, Ld["gate_up_f"], out=dec.gu, x_op=3, ssq_in=dec.ssq_b,
+            f"gemm_gate_up+rmsnorm+silu[{shapes['gate_up'][0]}x{shapes['gate_up'][1]}]:ImplB": (
+                lambda: [run_fused(dec.x, Ld["gate_up_f"], silu_out=dec.act, x_op=3, ssq_in=dec.ssq_b,
                                    ssq_tiles=st, eps=cfg.eps, ws_tag="decode_gemm")
                          for Ld in L0],
                 gb(*shapes["gate_up"]), len(L0)),

@@ -171,6 +171,11 @@ typedef struct fdpp_gemm_fuse {
     int32_t Hq, Hkv;
     int64_t cache_stride_b, cache_stride_h;
     float theta;
+    void *act_out;           /* optional SiLU*up epilogue (fused gate|up projection whose
+                                weight rows are tile-interleaved: each 128-row tile holds 64
+                                gate rows then the matching 64 up rows): act_out[m, 64 t + j]
+                                = silu(gate) * up, [M, N/2] with leading dim act_ld; C unused */
+    int64_t act_ld;
 } fdpp_gemm_fuse;
 
 /* ImplB with the fusions above (fused epilogues run in cluster split-K mode). */

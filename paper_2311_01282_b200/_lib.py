@@ -56,7 +56,7 @@ class GemmFuse(ctypes.Structure):
         ("norm_w", c_vp), ("eps", c_f32), ("ssq_out", c_vp), ("ssq_out_ld", c_i32),
         ("q_out", c_vp), ("k_cache", c_vp), ("v_cache", c_vp), ("pos", c_vp),
         ("Hq", c_i32), ("Hkv", c_i32), ("cache_stride_b", c_i64), ("cache_stride_h", c_i64),
-        ("theta", c_f32),
+        ("theta", c_f32), ("act_out", c_vp), ("act_ld", c_i64),
     ]
 
 

@@ -162,6 +162,8 @@ struct GemmFuse {
     int64_t cache_sb, cache_sh;
     float theta;
     int l2pf;                       // weight k-blocks prefetched to L2 ahead of the ring
+    void *act_out;                  // epilogue: silu(gate) * up of tile-interleaved gate|up rows
+    int64_t act_ld;
 };
 
 template <int BW, int BX, int STAGES, bool XF = false>
@@ -789,6 +791,10 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     } else {  // ---------------- epilogue warps: TMEM -> own smem partial [col][row]
         const int quad = warp & 3;
         const int row = quad * 32 + lane;
+        if (fz.x_op == 3) {  // folded RMSNorm: inverse RMS of the token rows, while the MMAs run
+            pdl_wait();      // the sums of squares come from the previous kernel
+            inv_rms_rows(s_inv_rms, M, K, fz, threadIdx.x - 64, 128);
+        }
         mbar_wait(tmem_full, 0);
         tc_fence_after();
 #pragma unroll 1
@@ -808,15 +814,12 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         const int quad = warp & 3;
         const int row = quad * 32 + lane;
         const int n = n0 + row;
-        if (fz.x_op == 3) {  // folded RMSNorm: inverse RMS of this CTA's token rows
-            inv_rms_rows(s_inv_rms, M, K, fz, threadIdx.x - 64, 128);
-            named_bar_sync(1, 128);
-        }
+        // (s_inv_rms was filled before the accumulator wait; the cluster barrier orders it)
         // column slice of this rank: a multiple of 4 columns (16-B DSMEM loads)
         const int per = (((MMA_N + ck.cs - 1) / ck.cs) + 3) & ~3;
         const int c_beg = (int)rank * per, c_end = min(MMA_N, c_beg + per);
-        const bool rope = fz.q_out != nullptr;
-        ClEpi<T> ep{part, rbuf, C, ldc, R, ldr, M, N, n0, m0, c_beg, c_end, row, lane, quad, rope,
+        const bool rope = fz.q_out != nullptr, silu = fz.act_out != nullptr;
+        ClEpi<T> ep{part, rbuf, C, ldc, R, ldr, M, N, n0, m0, c_beg, c_end, row, lane, quad, rope || silu,
                     fz.x_op == 3 ? s_inv_rms : nullptr, fz.ssq_out ? &s_ssq[0][0] : nullptr};
         switch (ck.cs) {
             case 2: cl_reduce_store<T, MMA_N, 2>(ep); break;
@@ -824,7 +827,18 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             case 8: cl_reduce_store<T, MMA_N, 8>(ep); break;
             default: cl_reduce_store_any<T, MMA_N>(ep, ck.cs); break;
         }
-        if (fz.ssq_out || rope) named_bar_sync(1, 128);
+        if (fz.ssq_out || rope || silu) named_bar_sync(1, 128);
+        if (silu && row < 64) {
+            // tile tn = gate rows [64 tn, 64 tn + 64) then the matching up rows; values
+            // staged rounded like the unfused gate|up buffer, then silu_mul's arithmetic
+            for (int c = c_beg; c < c_end; ++c) {
+                const int m = m0 + c;
+                if (m >= M) continue;
+                const float g = rbuf[(c - c_beg) * 128 + row], u = rbuf[(c - c_beg) * 128 + row + 64];
+                static_cast<T *>(fz.act_out)[(int64_t)m * fz.act_ld + tn * 64 + row] =
+                    Elem<T>::from_f(__fdividef(g, 1.f + __expf(-g)) * u);
+            }
+        }
         if (fz.ssq_out && row < c_end - c_beg) {
             const int m = m0 + c_beg + row;
             if (m < M)
@@ -1136,8 +1150,8 @@ static int l2_prefetch_blocks() {
 
 static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st,
                           const fdpp_gemm_fuse *fuse = nullptr) {
-    const bool epi_fuse = fuse && (fuse->ssq_out || fuse->q_out);
-    fdpp_status s = check_gemm(p, fuse && fuse->q_out);
+    const bool epi_fuse = fuse && (fuse->ssq_out || fuse->q_out || fuse->act_out);
+    fdpp_status s = check_gemm(p, fuse && (fuse->q_out || fuse->act_out));
     if (s != FDPP_OK) return s;
     TcPlan pl;
     fdpp_gemm_params q = *p;
@@ -1182,6 +1196,10 @@ static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st,
         L.fz.cache_sb = fuse->cache_stride_b;
         L.fz.cache_sh = fuse->cache_stride_h;
         L.fz.theta = fuse->theta;
+        FDPP_REQUIRE(!fuse->act_out || (p->N % 128 == 0 && !fuse->q_out && fuse->act_ld >= p->N / 2),
+                     FDPP_ERR_VALUE, "SiLU epilogue needs N %% 128 == 0 (tile-interleaved gate|up)");
+        L.fz.act_out = fuse->act_out;
+        L.fz.act_ld = fuse->act_ld;
     }
     if ((s = make_kmajor_map(&L.mw, p->w, p->N, p->K, p->ldw, pl.bw, p->dtype)) != FDPP_OK) return s;
     if ((s = make_kmajor_map(&L.mx, p->a, p->M, p->K, p->lda, pl.bx, p->dtype)) != FDPP_OK) return s;

@@ -163,9 +163,22 @@ def reference_call(impl: int, a, b, **kw):
     return c.float().cpu().numpy() if was_numpy else c
 
 
+def interleave_gate_up(pw: PackedWeight) -> PackedWeight:
+    """Rows of a fused [gate; up] weight (N = 2F, F % 64 == 0) reordered so each
+    128-row tile t holds gate rows [64t, 64t+64) then the matching up rows: the
+    layout the SiLU*up epilogue (run_fused(silu_out=...)) consumes."""
+    torch = _torch()
+    F = pw.N // 2
+    if pw.N % 128:
+        raise ShapeError(f"gate|up width {pw.N} must be a multiple of 128")
+    t = torch.arange(F // 64, device=pw.w.device)[:, None] * 64 + torch.arange(64, device=pw.w.device)[None, :]
+    idx = torch.stack([t, t + F], 1).reshape(-1)
+    return PackedWeight(pw.w[idx].contiguous(), pw.K, pw.N)
+
+
 def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ssq_in=None,
               ssq_tiles: int = 0, norm_w=None, eps: float = 1e-5, ssq_out=None, rope=None,
-              stream=None, ws_tag="gemm"):
+              silu_out=None, stream=None, ws_tag="gemm"):
     """ImplB with the decode-step fusions (fdpp_gemm_fused).
 
     x_op 1: the activation tile is RMSNorm(a) * norm_w, with the rows' sums of
@@ -174,7 +187,8 @@ def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ss
     ssq_out [N/128, M] (float32): per-128-column sums of squares of the stored
     output rows (for the next GEMM's x_op 1).  rope = dict(q_out, k_cache,
     v_cache, pos, theta): RoPE the q/k heads and append k/v at row pos[m]
-    (QKV projection; ``out`` unused)."""
+    (QKV projection; ``out`` unused).  silu_out [M, N/2]: silu(gate) * up of a
+    tile-interleaved gate|up weight (interleave_gate_up; ``out`` unused)."""
     torch = _torch()
     K = pw.ldw
     if x_op == 2:
@@ -183,7 +197,7 @@ def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ss
     elif a.shape[1] != K:
         raise ShapeError(f"inner dims disagree: {tuple(a.shape)} x [K={pw.K}, N={pw.N}]")
     M = a.shape[0]
-    if out is None and rope is None:
+    if out is None and rope is None and silu_out is None:
         out = torch.empty((M, pw.N), dtype=a.dtype, device=a.device)
     prm = _lib.GemmParams()
     prm.a, prm.lda = a.data_ptr(), a.stride(0)
@@ -210,6 +224,8 @@ def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ss
         fz.Hq, fz.Hkv = rope["q_out"].shape[1], kc.shape[1]
         fz.cache_stride_b, fz.cache_stride_h = kc.stride(0), kc.stride(1)
         fz.theta = float(rope.get("theta", 10000.0))
+    if silu_out is not None:
+        fz.act_out, fz.act_ld = silu_out.data_ptr(), silu_out.stride(0)
     lib = _lib.load()
     need = ctypes.c_size_t()
     _lib.check(lib.fdpp_gemm_workspace_size(IMPL_B, ctypes.byref(prm), ctypes.byref(need)), "gemm_fused")

@@ -30,7 +30,7 @@ import torch
 from . import _lib, tp as _tp, workspace
 from . import dispatch as _dispatch_mod  # noqa: F401  (module, not the function)
 from .attention import AttentionConfig, decode_attention
-from .gemm import PackedWeight, run_fused
+from .gemm import PackedWeight, interleave_gate_up, run_fused
 from .softmax import ScalingCalibration
 
 import importlib
@@ -197,12 +197,12 @@ class LlamaDecoder:
         if fused:  # fold the RMSNorm weights into the following projections' columns
             for L in self.layers:
                 L["qkv_f"] = fold_norm(L["qkv"], L["ln1"])
-                L["gate_up_f"] = fold_norm(L["gate_up"], L["ln2"])
+                L["gate_up_f"] = interleave_gate_up(fold_norm(L.pop("gate_up"), L["ln2"]))
             self.lm_head_f = fold_norm(self.lm_head, self.ln_f)
         self.fused = fused
-        # fused: embed + L x (qkv+rope, attn async, attn recompute, o, gate_up, silu, down
+        # fused: embed + L x (qkv+rope, attn async, attn recompute, o, gate_up+silu, down
         #        [+ 2 row-ssq after the all-reduces]) + lm_head + argmax + advance
-        per_layer = 7 + (2 if tp_size > 1 else 0)
+        per_layer = 6 + (2 if tp_size > 1 else 0)
         self.launches_per_step = (1 + self.n_layers * per_layer + 3) if fused else (1 + self.n_layers * 10 + 4)
 
     # ------------------------------------------------------------------ state
@@ -266,10 +266,8 @@ class LlamaDecoder:
                       ssq_out=None if tp else self.ssq_b, ws_tag="decode_gemm")
             if tp:
                 all_reduce_x(self.ssq_b)
-            run_fused(self.x, L["gate_up_f"], out=self.gu, x_op=3, ssq_in=self.ssq_b,
+            run_fused(self.x, L["gate_up_f"], x_op=3, ssq_in=self.ssq_b, silu_out=self.act,
                       ssq_tiles=1 if tp else self.ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
-            _lib.check(lib.fdpp_silu_mul(self.gu.data_ptr(), self.act.data_ptr(), B, self.ffn_local, dt,
-                                         st), "silu_mul")
             run_fused(self.act, L["down"], out=self.x, residual=self.x if lead else None,
                       ssq_out=None if tp else self.ssq_a, ws_tag="decode_gemm")
             if tp:

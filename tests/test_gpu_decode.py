@@ -199,3 +199,21 @@ def test_row_ssq(torch, mods):
     torch.cuda.synchronize()
     ref = (x.float() ** 2).sum(1)
     assert torch.allclose(out, ref, rtol=1e-5)
+
+
+def test_fused_silu_epilogue(torch, mods):
+    """gate|up GEMM with the SiLU*up epilogue (tile-interleaved weight rows) ==
+    the plain fused GEMM into [gate | up] followed by the silu_mul kernel."""
+    fd, _lib, gemm, _, D = mods
+    for B, H, F in ((32, 4096, 11008), (5, 1024, 1536)):
+        g = torch.Generator(device="cuda").manual_seed(B)
+        x = torch.randn((B, H), generator=g, device="cuda").half()
+        w = (torch.randn((2 * F, H), generator=g, device="cuda") / math.sqrt(H)).half()
+        pw = fd.PackedWeight(w, H, 2 * F)
+        gu = gemm.run_fused(x, pw)
+        act_ref = torch.empty((B, F), device="cuda", dtype=torch.half)
+        _lib.check(_lib.load().fdpp_silu_mul(gu.data_ptr(), act_ref.data_ptr(), B, F, 0, _lib.stream_handle()))
+        act = torch.empty_like(act_ref)
+        gemm.run_fused(x, gemm.interleave_gate_up(pw), silu_out=act)
+        torch.cuda.synchronize()
+        assert _rel(act, act_ref) <= 2e-3
