@@ -218,6 +218,13 @@ fdpp_status fdpp_embed(const int32_t *ids, const void *table, void *out, int32_t
  * all-reduce of the residual stream. */
 fdpp_status fdpp_row_ssq(const void *x, float *ssq_out, int32_t B, int32_t dim, int32_t dtype,
                          void *stream);
+
+/* Calibration producer: out[i] = scale * q[b,h] . k[b, h/G, key] at n
+ * pseudo-random (b, h, key < seq_lens[b]) drawn from `seed` (uses p's q, k, strides,
+ * seq_lens, B, Hq, Hkv, L, D, scale, dtype); idx_out (optional) [n][3] = (b, h, key).
+ * The host fits phi and the band with calibrate() (softmax.py:219-266). */
+fdpp_status fdpp_sample_logits(const fdpp_attn_params *p, int32_t n, uint64_t seed, float *out,
+                               int32_t *idx_out, void *stream);
 /* ids[r] = argmax_j logits[r, j] (lowest index on ties). */
 fdpp_status fdpp_argmax(const void *logits, int32_t *ids, int32_t rows, int32_t vocab,
                         int32_t dtype, void *stream);

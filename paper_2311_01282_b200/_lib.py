@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libfdpp.so")
+LIB_PATH = os.environ.get("FDPP_LIB") or os.path.join(_HERE, "_lib", "libfdpp.so")  # FDPP_LIB: dev override
 
 F16, BF16, F32 = 0, 1, 2
 ATTN_ASYNC, ATTN_SYNC = 0, 1
@@ -88,6 +88,7 @@ SIGNATURES = {
     "fdpp_silu_mul": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_embed": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_i32, c_vp]),
     "fdpp_row_ssq": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
+    "fdpp_sample_logits": (c_i32, [ctypes.POINTER(AttnParams), c_i32, ctypes.c_uint64, c_vp, c_vp, c_vp]),
     "fdpp_argmax": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_advance_positions": (c_i32, [c_vp, c_vp, c_i32, c_vp]),
 }

@@ -362,3 +362,27 @@ def async_chunk_state(q, K, V, lo: int, hi: int, cfg: AttentionConfig) -> Partia
     num, den, viol = async_partials(_row(q), Kc, Vc, one)
     v = int(viol[0, 0])
     return PartialAttnState(num[0, 0], np.float32(den[0, 0]), v + lo if v >= 0 else -1)
+
+
+def sample_logits(q, k_cache, scale: float, n: int, *, seq_lens=None, seed: int = 0,
+                  return_index: bool = False):
+    """Calibration producer: ``n`` logits
+    ``scale * q[b, h] . k[b, h // G, key]`` at pseudo-random (b, h, key < seq_lens[b])
+    computed on the device (``fdpp_sample_logits``) -- the sample the
+    reference's ``calibrate`` (softmax.py:219-266) fits phi and the band to.
+    Returns a float32 CUDA tensor (and the [n, 3] int32 (b, h, key) indices)."""
+    torch = _torch()
+    _lib.require_cuda()
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    prm = _params(q, k_cache, k_cache, q, AttentionConfig(p=0, scale=scale), "sync", None)
+    if seq_lens is not None:
+        if seq_lens.dtype != torch.int32 or not seq_lens.is_cuda:
+            raise ValueError("seq_lens must be an int32 CUDA tensor")
+        prm.seq_lens = seq_lens.data_ptr()
+    out = torch.empty(n, dtype=torch.float32, device=q.device)
+    idx = torch.empty((n, 3), dtype=torch.int32, device=q.device) if return_index else None
+    _lib.check(_lib.load().fdpp_sample_logits(ctypes.byref(prm), int(n), int(seed) & (2 ** 64 - 1),
+                                              out.data_ptr(), idx.data_ptr() if idx is not None else None,
+                                              _lib.stream_handle()), "sample_logits")
+    return (out, idx) if return_index else out

@@ -133,6 +133,47 @@ __global__ void row_ssq_kernel(const T *__restrict__ x, int dim, float *__restri
     }
 }
 
+// Calibration producer: n logits s = scale * q[b, h] . k[b, h/G, key]
+// at pseudo-random (b, h, key < lens[b]) -- the sample the reference's
+// calibrate() (softmax.py:219-266) fits phi and the band to.  One warp per sample.
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    return x ^ (x >> 33);
+}
+
+template <typename T>
+__global__ void sample_logits_kernel(const T *__restrict__ q, const T *__restrict__ k,
+                                     const int32_t *__restrict__ lens, int B, int Hq, int Hkv, int D,
+                                     int L, int64_t q_sb, int64_t q_sh, int64_t kv_sb, int64_t kv_sh,
+                                     float scale, int n, uint64_t seed, float *__restrict__ out,
+                                     int32_t *__restrict__ idx_out) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const uint64_t r = mix64(seed * 0x9e3779b97f4a7c15ull + (uint64_t)i);
+    const int b = (int)(r % (uint64_t)B);
+    const int h = (int)((r >> 20) % (uint64_t)Hq);
+    const int Lb = lens ? min(lens[b], L) : L;
+    const int key = (int)((r >> 40) % (uint64_t)max(Lb, 1));
+    const T *qp = q + (int64_t)b * q_sb + (int64_t)h * q_sh;
+    const T *kp = k + (int64_t)b * kv_sb + (int64_t)(h / (Hq / Hkv)) * kv_sh + (int64_t)key * D;
+    float acc = 0.f;
+    for (int d = lane; d < D; d += 32) acc = fmaf(Elem<T>::to_f(qp[d]), Elem<T>::to_f(kp[d]), acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+        out[i] = scale * acc;
+        if (idx_out) {
+            idx_out[3 * i] = b;
+            idx_out[3 * i + 1] = h;
+            idx_out[3 * i + 2] = key;
+        }
+    }
+}
+
 template <typename T>
 __global__ void argmax_kernel(const T *__restrict__ logits, int32_t *__restrict__ ids, int vocab) {
     pdl_wait();
@@ -243,6 +284,24 @@ extern "C" fdpp_status fdpp_row_ssq(const void *x, float *ssq_out, int32_t B, in
     FDPP_DT_SWITCH(dtype, e = launch_kernel(row_ssq_kernel<T>, dim3(B), dim3(256), 0, st,
                                             static_cast<const T *>(x), (int)dim, ssq_out));
     if (e != cudaSuccess) return cuda_status(e, "row_ssq_kernel launch");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_sample_logits(const fdpp_attn_params *p, int32_t n, uint64_t seed,
+                                          float *out, int32_t *idx_out, void *stream) {
+    FDPP_REQUIRE(p && out && p->q && p->k, FDPP_ERR_VALUE, "null pointer");
+    FDPP_REQUIRE(n >= 1 && p->B >= 1 && p->Hq >= 1 && p->Hkv >= 1 && p->Hq % p->Hkv == 0 && p->L >= 1 &&
+                     p->D >= 1, FDPP_ERR_SHAPE, "sample_logits dims");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaSuccess;
+    const int per_block = 8;  // warps (samples) per 256-thread block
+    FDPP_DT_SWITCH(p->dtype, e = launch_kernel(sample_logits_kernel<T>, dim3((n + per_block - 1) / per_block),
+                                               dim3(32 * per_block), 0, st, static_cast<const T *>(p->q),
+                                               static_cast<const T *>(p->k), p->seq_lens, (int)p->B,
+                                               (int)p->Hq, (int)p->Hkv, (int)p->D, (int)p->L, p->q_stride_b,
+                                               p->q_stride_h, p->kv_stride_b, p->kv_stride_h, p->scale,
+                                               (int)n, (uint64_t)seed, out, idx_out));
+    if (e != cudaSuccess) return cuda_status(e, "sample_logits_kernel launch");
     return FDPP_OK;
 }
 

@@ -194,6 +194,7 @@ class LlamaDecoder:
         if tp_size > 1 and not fused:
             raise NotImplementedError("tensor parallelism runs on the fused (ImplB) decode step")
         self.graph = None
+        self._layer_hook = None  # calibrate(): samples attention inputs after each QKV
         if fused:  # fold the RMSNorm weights into the following projections' columns
             for L in self.layers:
                 L["qkv_f"] = fold_norm(L["qkv"], L["ln1"])
@@ -204,6 +205,39 @@ class LlamaDecoder:
         #        [+ 2 row-ssq after the all-reduces]) + lm_head + argmax + advance
         per_layer = 6 + (2 if tp_size > 1 else 0)
         self.launches_per_step = (1 + self.n_layers * per_layer + 3) if fused else (1 + self.n_layers * 10 + 4)
+
+    # ------------------------------------------------------------------ calibration
+    def calibrate(self, target_coverage: float = 0.9999, margin: float = 1.0, samples_per_layer: int = 65536,
+                  seed: int = 0, apply: bool = True) -> ScalingCalibration:
+        """Fit the unified phi and band to this model's logits:
+        one eager decode step whose attention inputs (RoPE'd q, the KV cache with
+        the new row) are sampled on the device after every layer's QKV projection
+        (attention.sample_logits), then the reference's calibrate (softmax.py:219-266)
+        on the host.  The step's state changes (positions, tokens, KV rows) are undone."""
+        import numpy as np
+        from .attention import sample_logits
+        from .softmax import calibrate as _calibrate
+        saved = (self.pos.clone(), self.lens.clone(), self.ids.clone())
+        samples = []
+
+        def hook(li):
+            samples.append(sample_logits(self.q, self.k_cache[li], self.attn_cfg.scale, samples_per_layer,
+                                         seq_lens=self.lens, seed=seed * 1000003 + li))
+        self._layer_hook = hook
+        try:
+            self.enqueue_step()
+        finally:
+            self._layer_hook = None
+        torch.cuda.synchronize()
+        self.pos.copy_(saved[0])
+        self.lens.copy_(saved[1])
+        self.ids.copy_(saved[2])
+        cal = _calibrate(torch.cat(samples).cpu().numpy().astype(np.float32), target_coverage, margin)
+        if apply:
+            self.attn_cfg = AttentionConfig(p=self.attn_cfg.p, scale=self.attn_cfg.scale, calib=cal,
+                                            splits_per_chunk=self.attn_cfg.splits_per_chunk)
+            self.graph = None  # the captured step holds the old calibration
+        return cal
 
     # ------------------------------------------------------------------ state
     def prefill_random(self, L: int, seed: int = 1):
@@ -260,6 +294,8 @@ class LlamaDecoder:
                       eps=cfg.eps, ws_tag="decode_gemm",
                       rope={"q_out": self.q, "k_cache": kc, "v_cache": vc, "pos": self.pos,
                             "theta": cfg.rope_theta})
+            if self._layer_hook is not None:
+                self._layer_hook(li)
             decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
                              seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed)
             run_fused(self.attn.view(B, Hq * Dh), L["o"], out=self.x, residual=self.x if lead else None,
@@ -296,6 +332,8 @@ class LlamaDecoder:
                                             vc.data_ptr(), self.pos.data_ptr(), B, Hq, Hkv, Dh,
                                             kc.stride(0), kc.stride(1), cfg.rope_theta, dt, st),
                        "rope_append")
+            if self._layer_hook is not None:
+                self._layer_hook(li)
             decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
                              seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed)
             self._gemm("o", self.attn.view(B, Hq * Dh), L["o"], self.x, residual=self.x)

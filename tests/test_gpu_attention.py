@@ -216,3 +216,20 @@ def test_errors(fd):
     with pytest.raises(ValueError):
         fd.batch_decode_attention(Q, np.ones((4, 8), np.float32), np.ones((4, 8), np.float32),
                                   fd.AttentionConfig(p=9, scale=1.0), "sync")
+
+
+def test_sample_logits_and_calibrate(fd, torch):
+    """Calibration producer: device-sampled logits equal scale * q . k at the
+    returned indices; calibrate() on them covers the sample (softmax.py:219-266)."""
+    B, Hq, Hkv, L, D = 3, 8, 2, 300, 128
+    q, k, _ = _qkv(torch, B, Hq, Hkv, L, D, 11, torch.float16)
+    lens = torch.tensor([300, 17, 123], dtype=torch.int32, device="cuda")
+    s, idx = fd.sample_logits(q, k, 0.125, 4096, seq_lens=lens, seed=3, return_index=True)
+    idx = idx.long().cpu()
+    assert (idx[:, 2] < lens.cpu()[idx[:, 0]].long()).all()
+    G = Hq // Hkv
+    ref = 0.125 * (q.float()[idx[:, 0], idx[:, 1]] * k.float()[idx[:, 0], idx[:, 1] // G, idx[:, 2]]).sum(-1)
+    assert torch.allclose(s.cpu(), ref.cpu(), rtol=1e-5, atol=1e-5)
+    cal = fd.calibrate(s.cpu().numpy(), 0.9999, 1.0)
+    x = s.cpu().numpy() - cal.phi
+    assert ((x > cal.a) & (x < cal.b)).mean() >= 0.9999

@@ -217,3 +217,17 @@ def test_fused_silu_epilogue(torch, mods):
         gemm.run_fused(x, gemm.interleave_gate_up(pw), silu_out=act)
         torch.cuda.synchronize()
         assert _rel(act, act_ref) <= 2e-3
+
+
+def test_decoder_calibrate(torch, mods):
+    """LlamaDecoder.calibrate(): fits phi / band to the model's own attention
+    logits, restores the decode state, and the recalibrated step flags nothing."""
+    fd, _lib, gemm, llama, D = mods
+    dec = _decoder(torch, mods, fused=True, layers=2, B=4, L=64)
+    pos0, ids0 = dec.pos.clone(), dec.ids.clone()
+    cal = dec.calibrate(samples_per_layer=8192)
+    assert torch.equal(dec.pos, pos0) and torch.equal(dec.ids, ids0)
+    assert cal.a < 0 < cal.b and dec.attn_cfg.calib == cal
+    dec.enqueue_step()
+    torch.cuda.synchronize()
+    assert int(dec.recomputed.item()) == 0
