@@ -59,6 +59,7 @@ struct AttnArgs {
     int *flag_mark;   // [B*Hkv] dedupe markers
     int *flag_count;  // [0] entries, [32] CTAs done (reset by the recompute launch)
     bool list_mode;
+    bool cluster_join;  // MMA async: the P CTAs of a row group are one cluster (DSMEM join)
 };
 
 template <typename T, int D>
@@ -145,6 +146,18 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
 // 16-key slice S = Q K^T, the unified-phi band check and e^(x - phi) in fp32
 // (exp-sums stay fp32), P = e * pscale packed to 16 bits as the next MMA's A
 // operand straight from the accumulators, O += P V.
+#ifdef FDPP_ATRACE
+// dev trace build only: per-CTA globaltimer stamps of the async launch (tools/attn_trace.py)
+__device__ unsigned long long g_atrace[8192][8];
+#define ATRACE(slot)                                                                      \
+    do {                                                                                  \
+        const unsigned cid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+        if (ASYNC && cid < 8192) g_atrace[cid][slot] = globaltimer_ns();                   \
+    } while (0)
+#else
+#define ATRACE(slot) do { } while (0)
+#endif
+
 // append (batch, kv-head) to the recompute list once per launch
 __device__ __forceinline__ void flag_group(const AttnArgs &a, int b, int kvh) {
     if (!a.flag_list) return;
@@ -163,9 +176,9 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
 
     extern __shared__ __align__(128) uint8_t smem_raw[];
     // the MMA path's TMA swizzle needs 1024-byte aligned stages
-    uint8_t *smem = MMA ? reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                                      ~uintptr_t(1023))
-                        : smem_raw;
+    // (an integer offset from the shared array keeps the pointer in the shared
+    // window, so every access below compiles to LDS/STS, not generic LD/ST)
+    uint8_t *smem = MMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + ATT_STAGES * Gm::STAGE_BYTES);
     uint64_t *empty = full + ATT_STAGES;
     float *red = reinterpret_cast<float *>(empty + ATT_STAGES);  // [NRED][GT][D+2]
@@ -185,7 +198,9 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     const int gcount = min(GT, args.G - g0);
     const int h0 = kvh * args.G + g0;         // first query head of this row group
 
+    if (threadIdx.x == 0) ATRACE(0);
     pdl_wait();  // q, the appended K/V row and row_flags come from earlier kernels
+    if (threadIdx.x == 0) ATRACE(1);
     if (!ASYNC && args.only_flagged) {        // recompute launch: skip clean row groups
         int any = 0;
         for (int g = 0; g < gcount; ++g) any |= args.row_flags[(int64_t)b * args.Hq + h0 + g];
@@ -216,6 +231,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     __syncthreads();
 
     const int row0 = b * args.Hq + h0;        // global row index of g = 0
+    if (threadIdx.x == 0) ATRACE(2);
 
     if (warp == ATT_CONSUMERS) {
         // ------------------------------------------------ producer warp
@@ -243,6 +259,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                     bulk_g2s(dv, vbase + (int64_t)key0 * D, bytes, &full[s], kEvictFirst);
                 }
             }
+            ATRACE(7);
         }
     } else if constexpr (MMA) {
         // ------------------------------------------------ consumer warps, tensor cores
@@ -377,6 +394,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
             viol0 = min(viol0, __shfl_xor_sync(0xffffffffu, viol0, off));
             viol1 = min(viol1, __shfl_xor_sync(0xffffffffu, viol1, off));
         }
+        if (threadIdx.x == 0) ATRACE(6);
         pdl_trigger();  // main stream done: the next kernel may start its prologue
         if constexpr (!ASYNC) {
             // per-warp partials (num, den, running max) for the Eq. (2) merge below
@@ -398,13 +416,21 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
 #pragma unroll 1
         for (int w = 0; w < ATT_CONSUMERS; ++w) {
             if (warp == w) {
+                // this thread's 2-float pairs: all earlier sums loaded first, then stored
+                float2 prev[D / 8][2];
 #pragma unroll
                 for (int nb = 0; nb < D / 8; ++nb)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        float *dst = red + (r0 + (i >> 1) * 8) * (D + 2) + 8 * nb + cq + (i & 1);
-                        *dst = (w == 0 ? 0.f : *dst) + o[nb][i] * ips;
-                    }
+                    for (int h = 0; h < 2; ++h)
+                        prev[nb][h] = w == 0 ? make_float2(0.f, 0.f)
+                                             : *reinterpret_cast<const float2 *>(
+                                                   red + (r0 + h * 8) * (D + 2) + 8 * nb + cq);
+#pragma unroll
+                for (int nb = 0; nb < D / 8; ++nb)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        *reinterpret_cast<float2 *>(red + (r0 + h * 8) * (D + 2) + 8 * nb + cq) =
+                            make_float2(prev[nb][h].x + o[nb][2 * h] * ips, prev[nb][h].y + o[nb][2 * h + 1] * ips);
                 if ((lane & 3) == 0) {
                     float *d0 = red + r0 * (D + 2), *d1 = red + (r0 + 8) * (D + 2);
                     d0[D] = (w == 0 ? 0.f : d0[D]) + den0;
@@ -523,6 +549,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                 }
             }
         }
+        if (threadIdx.x == 0) ATRACE(6);
         pdl_trigger();  // main stream done: the next kernel may start its prologue
         // ---- per-warp partials to shared memory: red[w][g][0..D) = num, [D] = den, [D+1] = m/viol
         if (kg == 0) {
@@ -539,6 +566,56 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
         }
     }
     __syncthreads();
+
+    if constexpr (MMA && ASYNC) {
+        if (args.cluster_join) {
+            // The P CTAs of this row group form one thread-block cluster (rank = chunk j,
+            // nsub = 1): the join reads the peers' [GT][D+2] partials over DSMEM instead of
+            // publishing to global memory for a last-arriving CTA to re-read (that join was
+            // per-CTA-bandwidth bound: P x GT x D x 4 bytes through one CTA).  Rank r joins
+            // rows r, r + P, ...; chunk sums in chunk (= rank) order as the global join.
+            __shared__ float s_dsum;
+            cluster_sync_all();  // every rank's partial is in its shared memory
+            const uint32_t red_addr = smem_u32(red);
+            const int rank = (int)cluster_ctarank();
+            for (int g = rank; g < gcount; g += P) {  // uniform per CTA
+                const int64_t row = row0 + g;
+                const uint32_t ra = red_addr + (uint32_t)(g * (D + 2)) * 4u;
+                int bad = 0;
+                float acc = 0.f;
+                if (threadIdx.x < D) {
+                    for (int q = 0; q < P; ++q) {  // chunk order
+                        const float v = dsmem_ld_f32(dsmem_map_addr(ra + 4u * threadIdx.x, q));
+                        bad |= !isfinite(v);
+                        acc += v;
+                    }
+                } else if (threadIdx.x == D) {
+                    float dsum = 0.f;
+                    for (int q = 0; q < P; ++q) {
+                        const float dq = dsmem_ld_f32(dsmem_map_addr(ra + 4u * D, q));
+                        const int vq = __float_as_int(dsmem_ld_f32(dsmem_map_addr(ra + 4u * (D + 1), q)));
+                        bad |= (vq != INT_MAX) || !isfinite(dq);  // non-finite chunk state = violation
+                        dsum += dq;
+                    }
+                    s_dsum = dsum;
+                }
+                const bool flagged = __syncthreads_or(bad) != 0;
+                if (threadIdx.x == 0) {
+                    args.row_flags[row] = flagged ? 1 : 0;
+                    if (flagged) {
+                        if (args.rows_recomputed) atomicAdd(args.rows_recomputed, 1);
+                        flag_group(args, b, kvh);
+                    }
+                }
+                if (!flagged && threadIdx.x < D)
+                    static_cast<T *>(args.o)[(int64_t)b * args.o_sb + (int64_t)(h0 + g) * args.o_sh + threadIdx.x] =
+                        Elem<T>::from_f(acc / s_dsum);
+                __syncthreads();  // s_dsum is rewritten by the next row
+            }
+            cluster_sync_all();  // peers may still be reading this CTA's partial
+            return;
+        }
+    }
 
     // ---- merge the consumer warps in fixed order and write this CTA's partial
     for (int idx = threadIdx.x; idx < gcount * (D + 2); idx += ATT_THREADS) {
@@ -574,6 +651,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     }
 
     // ---- last CTA of the row group joins all partials (fixed order)
+    if (threadIdx.x == 0) ATRACE(3);
     __threadfence();
     __syncthreads();
     const int counter = (b * args.Hkv + kvh) * args.n_rg + rg;
@@ -583,6 +661,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
         if (s_last) args.counters[counter] = 0;
     }
     __syncthreads();
+    if (threadIdx.x == 0) ATRACE(4);
     if (!s_last) return;
     __threadfence();
     if (ASYNC) {
@@ -606,27 +685,40 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                 int vm = INT_MAX;
                 for (int q = 0; q < nsub; ++q) {
                     const int64_t i = base + (int64_t)jj * nsub + q;
-                    cd += ld_cg_f32(&args.ws_den[i]);
+                    cd += __ldcg(&args.ws_den[i]);
                     vm = min(vm, __ldcg(&args.ws_viol[i]));
                 }
                 bad |= vm != INT_MAX || !isfinite(cd);  // a non-finite chunk state is a violation
                 dpart += cd;
             }
-            // numerators: chunk sums in sub order, totals in chunk order
+            // numerators: chunk sums in sub order, totals in chunk order.  Lane owns
+            // D / 32 consecutive d (one 16-B load per slot at D = 128); LBW slots in flight
             constexpr int NDL = (D + 31) / 32;
+            constexpr bool V4 = (D % 128 == 0) && NDL == 4;
             float acc[NDL], cn[NDL];
 #pragma unroll
             for (int r = 0; r < NDL; ++r) acc[r] = cn[r] = 0.f;
-            constexpr int LBW = 8;
+            constexpr int LBW = V4 ? 16 : 8;
             for (int i0 = 0; i0 < P; i0 += LBW) {
                 float val[LBW][NDL];
 #pragma unroll
-                for (int q = 0; q < LBW; ++q)
+                for (int q = 0; q < LBW; ++q) {
+                    if constexpr (V4) {
+                        const float4 t4 = i0 + q < P ? __ldcg(reinterpret_cast<const float4 *>(
+                                                           &args.ws_num[(base + i0 + q) * D + 4 * lane]))
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                        val[q][0] = t4.x;
+                        val[q][1] = t4.y;
+                        val[q][2] = t4.z;
+                        val[q][3] = t4.w;
+                    } else {
 #pragma unroll
-                    for (int r = 0; r < NDL; ++r) {
-                        const int d = lane + 32 * r;
-                        val[q][r] = (i0 + q < P && d < D) ? ld_cg_f32(&args.ws_num[(base + i0 + q) * D + d]) : 0.f;
+                        for (int r = 0; r < NDL; ++r) {
+                            const int d = lane + 32 * r;
+                            val[q][r] = (i0 + q < P && d < D) ? __ldcg(&args.ws_num[(base + i0 + q) * D + d]) : 0.f;
+                        }
                     }
+                }
 #pragma unroll
                 for (int q = 0; q < LBW; ++q) {
                     if (i0 + q >= P) break;
@@ -655,12 +747,15 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
             if (!flagged) {
                 T *op = static_cast<T *>(args.o) + (int64_t)b * args.o_sb + (int64_t)(h0 + g) * args.o_sh;
 #pragma unroll
-                for (int r = 0; r < NDL; ++r)
-                    if (lane + 32 * r < D) op[lane + 32 * r] = Elem<T>::from_f(acc[r] / dpart);
+                for (int r = 0; r < NDL; ++r) {
+                    const int d = V4 ? 4 * lane + r : lane + 32 * r;
+                    if (d < D) op[d] = Elem<T>::from_f(acc[r] / dpart);
+                }
             }
         }
         __syncthreads();
         if (threadIdx.x == 0 && s_grp_flag) flag_group(args, b, kvh);
+        if (threadIdx.x == 0) ATRACE(5);
         return;
     }
     constexpr int LB = 32;  // partial loads kept in flight per thread
@@ -906,8 +1001,8 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
         // second partial wave, >= 128 keys per CTA (profiles/r1_attn_gqa_sweep.txt)
         int want = (3 * sms) / launch_groups;
         int maxp = p->L / 128 > 0 ? p->L / 128 : 1;
+        if (maxp > 16) maxp = 16;  // the cluster (DSMEM) join takes <= 16 CTAs per row group
         lay->p = want < 1 ? 1 : (want > maxp ? maxp : want);
-        if (lay->p > ATT_MAX_P) lay->p = ATT_MAX_P;
     } else {
         // auto: enough chunks for ~8 CTAs per SM over the launch, >= 512 keys each
         int want = (8 * sms + launch_groups - 1) / launch_groups;
@@ -922,7 +1017,9 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
     } else {
         const int per_chunk = p->L / lay->p;
         int want = (8 * sms + launch_groups * lay->p - 1) / (launch_groups * lay->p);
-        int maxs = per_chunk / 512 > 0 ? per_chunk / 512 : 1;  // >= 512 keys per CTA
+        // >= 128 keys per CTA: few (batch, kv-head) groups (config 1: B = 1) need the
+        // splits to fill the machine; with many groups the CTA target is met first
+        int maxs = per_chunk / 128 > 0 ? per_chunk / 128 : 1;
         lay->nsub = want < 1 ? 1 : (want > maxs ? maxs : want);
     }
     lay->P = lay->p * lay->nsub;
@@ -954,13 +1051,16 @@ static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st,
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e == cudaSuccess && MMA)  // cluster join: up to 16 CTAs per cluster
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn)");
         attr = true;
     }
-    // list_mode: grid_x CTAs walk the flagged-group list
+    // list_mode: grid_x CTAs walk the flagged-group list; cluster_join: the grid_x
+    // (= P) CTAs of a row group are one cluster
     dim3 grid = a.list_mode ? dim3(grid_x) : dim3(grid_x, a.Hkv * a.n_rg, a.B);
-    cudaError_t e = launch_kernel(kern, grid, dim3(ATT_THREADS), smem, st, a, tmK ? *tmK : none,
-                                  tmV ? *tmV : none);
+    cudaError_t e = launch_kernel_cluster(kern, grid, dim3(ATT_THREADS), smem, st, a.cluster_join ? grid_x : 1,
+                                          a, tmK ? *tmK : none, tmV ? *tmV : none);
     if (e != cudaSuccess) return cuda_status(e, "attn_split_kernel launch");
     return FDPP_OK;
 }
@@ -1024,6 +1124,16 @@ static fdpp_status by_dtype(const AttnArgs &a, int dtype, int D, int gt, int gx,
 
 using namespace fdpp;
 
+#ifdef FDPP_ATRACE
+extern "C" int fdpp_atrace_read(unsigned long long *host) {
+    return (int)cudaMemcpyFromSymbol(host, fdpp::g_atrace, sizeof(fdpp::g_atrace));
+}
+extern "C" int fdpp_atrace_reset(void) {
+    static unsigned long long z[8192][8];
+    return (int)cudaMemcpyToSymbol(fdpp::g_atrace, z, sizeof(z));
+}
+#endif
+
 extern "C" fdpp_status fdpp_attn_workspace_size(const fdpp_attn_params *p, size_t *bytes) {
     FDPP_REQUIRE(bytes != nullptr, FDPP_ERR_VALUE, "null bytes");
     AttnLayout lay;
@@ -1086,6 +1196,7 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     a.flag_list = use_list ? flags + kFlagListOff : nullptr;
     a.flag_mark = flags + kFlagListOff + kFlagMax;
     a.list_mode = false;
+    a.cluster_join = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     a.kv_rows_per_head = p->kv_stride_h / p->D;
     const bool sync_mma = mma_shape_ok(p, lay.G);  // GQA/MQA sync softmax on tensor cores
@@ -1106,6 +1217,7 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     if (lay.mma) {
         AttnArgs am = a;
         am.n_rg = lay.n_rg_mma;
+        am.cluster_join = lay.P <= 16 && lay.nsub == 1 && !p->viol_index && !p->chunk_num && !p->chunk_den;
         am.pscale = lay.pscale;
         am.inv_pscale = 1.f / lay.pscale;
         s = launch_mma<true>(am, p->dtype, lay.P, &mk, &mv, st);
