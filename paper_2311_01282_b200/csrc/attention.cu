@@ -567,7 +567,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     }
     __syncthreads();
 
-    if constexpr (MMA && ASYNC) {
+    if constexpr (ASYNC) {
         if (args.cluster_join) {
             // The P CTAs of this row group form one thread-block cluster (rank = chunk j,
             // nsub = 1): the join reads the peers' [GT][D+2] partials over DSMEM instead of
@@ -583,17 +583,28 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                 const uint32_t ra = red_addr + (uint32_t)(g * (D + 2)) * 4u;
                 int bad = 0;
                 float acc = 0.f;
-                if (threadIdx.x < D) {
+                // a rank's chunk value = its NRED warp buffers summed in warp order
+                constexpr uint32_t WSTRIDE = GT * (D + 2) * 4u;
+                for (int d = threadIdx.x; d < D; d += ATT_THREADS) {
                     for (int q = 0; q < P; ++q) {  // chunk order
-                        const float v = dsmem_ld_f32(dsmem_map_addr(ra + 4u * threadIdx.x, q));
-                        bad |= !isfinite(v);
-                        acc += v;
+                        float cv = 0.f;
+#pragma unroll
+                        for (int w = 0; w < NRED; ++w)
+                            cv += dsmem_ld_f32(dsmem_map_addr(ra + w * WSTRIDE + 4u * d, q));
+                        bad |= !isfinite(cv);
+                        acc += cv;
                     }
-                } else if (threadIdx.x == D) {
+                }
+                if (threadIdx.x == ATT_THREADS - 1) {
                     float dsum = 0.f;
                     for (int q = 0; q < P; ++q) {
-                        const float dq = dsmem_ld_f32(dsmem_map_addr(ra + 4u * D, q));
-                        const int vq = __float_as_int(dsmem_ld_f32(dsmem_map_addr(ra + 4u * (D + 1), q)));
+                        float dq = 0.f;
+                        int vq = INT_MAX;
+#pragma unroll
+                        for (int w = 0; w < NRED; ++w) {
+                            dq += dsmem_ld_f32(dsmem_map_addr(ra + w * WSTRIDE + 4u * D, q));
+                            vq = min(vq, __float_as_int(dsmem_ld_f32(dsmem_map_addr(ra + w * WSTRIDE + 4u * (D + 1), q))));
+                        }
                         bad |= (vq != INT_MAX) || !isfinite(dq);  // non-finite chunk state = violation
                         dsum += dq;
                     }
@@ -607,7 +618,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                         flag_group(args, b, kvh);
                     }
                 }
-                if (!flagged && threadIdx.x < D)
+                if (!flagged && threadIdx.x < D)  // D <= ATT_THREADS on this path (host check)
                     static_cast<T *>(args.o)[(int64_t)b * args.o_sb + (int64_t)(h0 + g) * args.o_sh + threadIdx.x] =
                         Elem<T>::from_f(acc / s_dsum);
                 __syncthreads();  // s_dsum is rewritten by the next row
@@ -1022,6 +1033,13 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
         int maxs = per_chunk / 128 > 0 ? per_chunk / 128 : 1;
         lay->nsub = want < 1 ? 1 : (want > maxs ? maxs : want);
     }
+    if (p->p <= 0 && p->splits_per_chunk <= 0 && !lay->mma && lay->p * lay->nsub <= 16 &&
+        lay->p * lay->nsub <= p->L) {
+        // auto, CUDA-core path: make each CTA one semantic chunk, so the <= 16 CTAs of a
+        // row group can join over DSMEM as one cluster
+        lay->p *= lay->nsub;
+        lay->nsub = 1;
+    }
     lay->P = lay->p * lay->nsub;
     FDPP_REQUIRE(lay->P <= ATT_MAX_P, FDPP_ERR_VALUE,
                  "p x splits_per_chunk = %d exceeds %d partials per row", lay->P, ATT_MAX_P);
@@ -1051,7 +1069,7 @@ static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st,
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e == cudaSuccess && MMA)  // cluster join: up to 16 CTAs per cluster
+        if (e == cudaSuccess && ASYNC)  // cluster join: up to 16 CTAs per cluster
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(attn)");
         attr = true;
@@ -1222,7 +1240,10 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
         am.inv_pscale = 1.f / lay.pscale;
         s = launch_mma<true>(am, p->dtype, lay.P, &mk, &mv, st);
     } else {
-        s = by_dtype<true>(a, p->dtype, p->D, lay.GT, lay.P, st);
+        AttnArgs ac = a;
+        ac.cluster_join = lay.P <= 16 && lay.nsub == 1 && p->D <= ATT_THREADS && !p->viol_index &&
+                          !p->chunk_num && !p->chunk_den;
+        s = by_dtype<true>(ac, p->dtype, p->D, lay.GT, lay.P, st);
     }
     if (s != FDPP_OK) return s;
     // synchronized recompute of flagged rows (attention.py:283-285), always launched
