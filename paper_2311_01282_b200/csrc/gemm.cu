@@ -731,6 +731,7 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     float *rbuf = reinterpret_cast<float *>(smem + CS::PART);    // RoPE staging [cols][128]
     __shared__ float s_inv_rms[XF_MAX_M];
     __shared__ float s_ssq[4][MMA_N];
+    __shared__ int s_pos[MMA_N];  // RoPE epilogue: positions of this CTA's tokens
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -795,6 +796,10 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             pdl_wait();      // the sums of squares come from the previous kernel
             inv_rms_rows(s_inv_rms, M, K, fz, threadIdx.x - 64, 128);
         }
+        if (fz.q_out != nullptr && row < MMA_N) {  // RoPE positions, off the epilogue's critical path
+            pdl_wait();
+            s_pos[row] = m0 + row < M ? fz.pos[m0 + row] : 0;
+        }
         mbar_wait(tmem_full, 0);
         tc_fence_after();
 #pragma unroll 1
@@ -852,7 +857,7 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             for (int c = c_beg; c < c_end; ++c) {
                 const int m = m0 + c;
                 if (m >= M) continue;
-                const int p = fz.pos[m];
+                const int p = s_pos[c];
                 const float *xr = rbuf + (c - c_beg) * 128;
                 T *dst;
                 float val;
