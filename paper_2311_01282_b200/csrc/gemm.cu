@@ -45,55 +45,74 @@ __global__ void prepack_kernel(const T *__restrict__ b, T *__restrict__ w, int K
 // ============================================================ ImplA: GEMV (M <= 8)
 // CTA = NR weight rows x full K; its 8 warps split K (warp w takes 16-byte
 // chunks w*32+lane, stepping 256), so every weight byte is loaded once and the
-// activation chunk a lane holds is reused across the NR rows.
-constexpr int GEMV_NR = 8;
+// activation chunk a lane holds is reused across the NR rows.  NR shrinks as M
+// grows (8 / 4 / 2 rows for M <= 2 / 4 / 8) so the fp32 accumulators stay
+// in registers at >= 2 CTAs per SM, and each thread keeps two chunks of every
+// row in flight (2 x NR 16-B loads).
 constexpr int GEMV_WARPS = 8;
 
+template <int MR>
+struct GemvRows {
+    static constexpr int NR = MR <= 2 ? 8 : (MR <= 4 ? 4 : 2);
+};
+
 template <typename T, int MR>
-__global__ void __launch_bounds__(GEMV_WARPS * 32)
+__global__ void __launch_bounds__(GEMV_WARPS * 32, 2)
 gemv_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W, int64_t ldw,
             T *C, int64_t ldc, const T *R, int64_t ldr, int M, int N, int K) {
+    constexpr int NR = GemvRows<MR>::NR;
+    constexpr int STEP = GEMV_WARPS * 32;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * GEMV_NR;
+    const int n0 = blockIdx.x * NR;
     const int nchunks = K >> 3;  // 8 elements per 16-B chunk (K % 8 == 0 by contract)
     pdl_wait();
-    float acc[GEMV_NR][MR];
+    float acc[NR][MR];
 #pragma unroll
-    for (int r = 0; r < GEMV_NR; ++r)
+    for (int r = 0; r < NR; ++r)
 #pragma unroll
         for (int m = 0; m < MR; ++m) acc[r][m] = 0.f;
 
-    const T *wrow[GEMV_NR];
+    const T *wrow[NR];
 #pragma unroll
-    for (int r = 0; r < GEMV_NR; ++r) wrow[r] = W + (int64_t)min(n0 + r, N - 1) * ldw;
+    for (int r = 0; r < NR; ++r) wrow[r] = W + (int64_t)min(n0 + r, N - 1) * ldw;
 
-    for (int c = warp * 32 + lane; c < nchunks; c += GEMV_WARPS * 32) {
-        int4 wv[GEMV_NR];
+    for (int c0 = warp * 32 + lane; c0 < nchunks; c0 += 2 * STEP) {
+        int4 wv[2][NR];
 #pragma unroll
-        for (int r = 0; r < GEMV_NR; ++r) wv[r] = ld_stream_16(wrow[r] + (int64_t)c * 8);
+        for (int h = 0; h < 2; ++h) {
+            const int c = c0 + h * STEP;
 #pragma unroll
-        for (int m = 0; m < MR; ++m) {
-            const int mm = m < M ? m : M - 1;  // rows past M are computed but never stored
-            int4 av = __ldg(reinterpret_cast<const int4 *>(A + (int64_t)mm * lda) + c);
-            float2 a0 = Elem<T>::to_f2(av.x), a1 = Elem<T>::to_f2(av.y);
-            float2 a2 = Elem<T>::to_f2(av.z), a3 = Elem<T>::to_f2(av.w);
+            for (int r = 0; r < NR; ++r)
+                wv[h][r] = c < nchunks ? ld_stream_16(wrow[r] + (int64_t)c * 8) : make_int4(0, 0, 0, 0);
+        }
 #pragma unroll
-            for (int r = 0; r < GEMV_NR; ++r) {
-                float2 w0 = Elem<T>::to_f2(wv[r].x), w1 = Elem<T>::to_f2(wv[r].y);
-                float2 w2 = Elem<T>::to_f2(wv[r].z), w3 = Elem<T>::to_f2(wv[r].w);
-                float s = acc[r][m];
-                s = fmaf(a0.x, w0.x, s); s = fmaf(a0.y, w0.y, s);
-                s = fmaf(a1.x, w1.x, s); s = fmaf(a1.y, w1.y, s);
-                s = fmaf(a2.x, w2.x, s); s = fmaf(a2.y, w2.y, s);
-                s = fmaf(a3.x, w3.x, s); s = fmaf(a3.y, w3.y, s);
-                acc[r][m] = s;
+        for (int h = 0; h < 2; ++h) {
+            const int c = c0 + h * STEP;
+            if (c >= nchunks) break;
+#pragma unroll
+            for (int m = 0; m < MR; ++m) {
+                const int mm = m < M ? m : M - 1;  // rows past M are computed but never stored
+                int4 av = __ldg(reinterpret_cast<const int4 *>(A + (int64_t)mm * lda) + c);
+                float2 a0 = Elem<T>::to_f2(av.x), a1 = Elem<T>::to_f2(av.y);
+                float2 a2 = Elem<T>::to_f2(av.z), a3 = Elem<T>::to_f2(av.w);
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    float2 w0 = Elem<T>::to_f2(wv[h][r].x), w1 = Elem<T>::to_f2(wv[h][r].y);
+                    float2 w2 = Elem<T>::to_f2(wv[h][r].z), w3 = Elem<T>::to_f2(wv[h][r].w);
+                    float s = acc[r][m];
+                    s = fmaf(a0.x, w0.x, s); s = fmaf(a0.y, w0.y, s);
+                    s = fmaf(a1.x, w1.x, s); s = fmaf(a1.y, w1.y, s);
+                    s = fmaf(a2.x, w2.x, s); s = fmaf(a2.y, w2.y, s);
+                    s = fmaf(a3.x, w3.x, s); s = fmaf(a3.y, w3.y, s);
+                    acc[r][m] = s;
+                }
             }
         }
     }
     pdl_trigger();
     // warp reduction (fixed butterfly order)
 #pragma unroll
-    for (int r = 0; r < GEMV_NR; ++r)
+    for (int r = 0; r < NR; ++r)
 #pragma unroll
         for (int m = 0; m < MR; ++m) {
             float v = acc[r][m];
@@ -101,15 +120,15 @@ gemv_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W, int64
             for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             acc[r][m] = v;
         }
-    __shared__ float red[GEMV_WARPS][GEMV_NR][MR];
+    __shared__ float red[GEMV_WARPS][NR][MR];
     if (lane == 0) {
 #pragma unroll
-        for (int r = 0; r < GEMV_NR; ++r)
+        for (int r = 0; r < NR; ++r)
 #pragma unroll
             for (int m = 0; m < MR; ++m) red[warp][r][m] = acc[r][m];
     }
     __syncthreads();
-    if (threadIdx.x < GEMV_NR * MR) {
+    if (threadIdx.x < NR * MR) {
         const int r = threadIdx.x / MR, m = threadIdx.x % MR, n = n0 + r;
         if (n < N && m < M) {
             float s = 0.f;
@@ -1231,7 +1250,8 @@ static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st,
 
 template <typename T>
 static fdpp_status launch_gemv(const fdpp_gemm_params *p, cudaStream_t st) {
-    dim3 grid(ceil_div(p->N, GEMV_NR));
+    const int nr = p->M <= 2 ? GemvRows<1>::NR : (p->M <= 4 ? GemvRows<4>::NR : GemvRows<8>::NR);
+    dim3 grid(ceil_div(p->N, nr));
     const T *A = static_cast<const T *>(p->a);
     const T *W = static_cast<const T *>(p->w);
     T *C = static_cast<T *>(p->c);
