@@ -431,6 +431,7 @@ def run_gpu(args):
                    "attention": f"async unified-phi, p={dec.attn_cfg.p or 'auto'}"
                                 + (", GQA/MQA on tensor cores" if cfg.n_heads // cfg.n_kv_heads >= 4 else ""),
                    "gemm_choices": {op: c.value for op, c in dec.choices.items()},
+                   "dispatch_table_choices": {op: c.value for op, c in dec.table_choices.items()},
                    "injected_groups_per_layer": args.inject},
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": B * 4,
                 "d2h_bytes_per_step": B * 4},

@@ -187,10 +187,16 @@ class LlamaDecoder:
         if table is None:
             table = build_dispatch_table(cfg, dtype=dtype, tp=tp_size)
         self.table = table
-        self.choices = {op: D.dispatch(B, n, k, table) for op, (n, k) in shapes.items()}
-        # the fused step is built on ImplB (prologue/epilogue fusions); use it when
-        # the dispatch table picks ImplB for every projection at this batch
-        fused = fused and all(c == D.KernelChoice.IMPL_B for c in self.choices.values())
+        # per-GEMM choice of the heuristic dispatch (the reference's decision flow)
+        self.table_choices = {op: D.dispatch(B, n, k, table) for op, (n, k) in shapes.items()}
+        # The fused step runs every projection on ImplB (its prologue/epilogue
+        # fusions remove the RMSNorm / RoPE / SiLU / residual kernels).  The table
+        # decides per GEMM; the step decides on the whole layer: at B = 1 the GEMV
+        # wins each GEMM in isolation (tables/b200_decode.tbl) but the unfused step
+        # is slower (profiles/r1_bench: 3.33 vs 2.80 ms).  ImplC (M beyond the
+        # flat-GEMM band) still forces the unfused step.
+        fused = fused and all(c != D.KernelChoice.IMPL_C for c in self.table_choices.values())
+        self.choices = ({op: D.KernelChoice.IMPL_B for op in shapes} if fused else dict(self.table_choices))
         if tp_size > 1 and not fused:
             raise NotImplementedError("tensor parallelism runs on the fused (ImplB) decode step")
         self.graph = None
