@@ -353,33 +353,34 @@ def run_gpu(args):
     gb = lambda n, k: n * k * 2 + B * k * 2 + B * n * 2  # noqa: E731
     if dec.fused:
         L0 = dec.layers
-        st = 1 if tp > 1 else dec.ssq_tiles
+        st = 1 if tp > 1 else (dec.gemv_ssq_tiles if dec.step_impl == "A" else dec.ssq_tiles)
+        im = dec.step_impl
         per_op = {
-            f"gemm_qkv+rmsnorm+rope[{shapes['qkv'][0]}x{shapes['qkv'][1]}]:ImplB": (
+            f"gemm_qkv+rmsnorm+rope[{shapes['qkv'][0]}x{shapes['qkv'][1]}]:Impl{im}": (
                 lambda: [run_fused(dec.x, Ld["qkv_f"], x_op=3, ssq_in=dec.ssq_a, ssq_tiles=st,
-                                   eps=cfg.eps, ws_tag="decode_gemm",
+                                   eps=cfg.eps, ws_tag="decode_gemm", impl=im,
                                    rope={"q_out": dec.q, "k_cache": dec.k_cache[i],
                                          "v_cache": dec.v_cache[i], "pos": dec.pos,
                                          "theta": cfg.rope_theta}) for i, Ld in enumerate(L0)],
                 gb(*shapes["qkv"]), len(L0)),
-            f"gemm_o+residual+ssq[{shapes['o'][0]}x{shapes['o'][1]}]:ImplB": (
+            f"gemm_o+residual+ssq[{shapes['o'][0]}x{shapes['o'][1]}]:Impl{im}": (
                 lambda: [run_fused(dec.attn.view(B, hq * dh), Ld["o"], out=dec.h, residual=dec.x,
-                                   ssq_out=None if tp > 1 else dec.ssq_b, ws_tag="decode_gemm")
+                                   ssq_out=None if tp > 1 else dec.ssq_b, ws_tag="decode_gemm", impl=im)
                          for Ld in L0],
                 gb(*shapes["o"]), len(L0)),
-            f"gemm_gate_up+rmsnorm+silu[{shapes['gate_up'][0]}x{shapes['gate_up'][1]}]:ImplB": (
+            f"gemm_gate_up+rmsnorm+silu[{shapes['gate_up'][0]}x{shapes['gate_up'][1]}]:Impl{im}": (
                 lambda: [run_fused(dec.x, Ld["gate_up_f"], silu_out=dec.act, x_op=3, ssq_in=dec.ssq_b,
-                                   ssq_tiles=st, eps=cfg.eps, ws_tag="decode_gemm")
+                                   ssq_tiles=st, eps=cfg.eps, ws_tag="decode_gemm", impl=im)
                          for Ld in L0],
                 gb(*shapes["gate_up"]), len(L0)),
-            f"gemm_down+residual+ssq[{shapes['down'][0]}x{shapes['down'][1]}]:ImplB": (
+            f"gemm_down+residual+ssq[{shapes['down'][0]}x{shapes['down'][1]}]:Impl{im}": (
                 lambda: [run_fused(dec.act, Ld["down"], out=dec.h, residual=dec.x,
-                                   ssq_out=None if tp > 1 else dec.ssq_a, ws_tag="decode_gemm")
+                                   ssq_out=None if tp > 1 else dec.ssq_a, ws_tag="decode_gemm", impl=im)
                          for Ld in L0],
                 gb(*shapes["down"]), len(L0)),
-            f"gemm_lm_head+rmsnorm[{shapes['lm_head'][0]}x{shapes['lm_head'][1]}]:ImplB": (
+            f"gemm_lm_head+rmsnorm[{shapes['lm_head'][0]}x{shapes['lm_head'][1]}]:Impl{im}": (
                 lambda: run_fused(dec.x, dec.lm_head_f, out=dec.logits, x_op=3, ssq_in=dec.ssq_a,
-                                  ssq_tiles=st, eps=cfg.eps, ws_tag="decode_gemm"),
+                                  ssq_tiles=st, eps=cfg.eps, ws_tag="decode_gemm", impl=im),
                 gb(*shapes["lm_head"]), 1),
         }
     else:

@@ -181,6 +181,14 @@ typedef struct fdpp_gemm_fuse {
 /* ImplB with the fusions above (fused epilogues run in cluster split-K mode). */
 fdpp_status fdpp_gemm_fused(const fdpp_gemm_params *p, const fdpp_gemm_fuse *fuse, void *stream);
 
+/* ImplA (GEMV, M <= 2) with the same fusions in GEMV form: x_op 0 or 3 (the inverse RMS
+ * comes from the activation rows the CTA streams; ssq_in is ignored), residual,
+ * ssq_out as one tile per 8 output columns (ssq_tiles = N / 8 for the consumer),
+ * RoPE + KV append for a QKV weight whose head rows are permuted to
+ * [4j..4j+3, 64+4j..64+4j+3] per 8-row block, SiLU*up for a gate|up weight permuted
+ * to [gate 4c..4c+3, up 4c..4c+3] per 8-row block (act_out [M, N/2]). */
+fdpp_status fdpp_gemv_fused(const fdpp_gemm_params *p, const fdpp_gemm_fuse *fuse, void *stream);
+
 /* ------------------------------------------ subsystem 3: heuristic dispatch */
 /* dispatch(m, n, k, table) on one entry (dispatch.py:189-197): 0=A,1=B,2=C. */
 int32_t fdpp_dispatch_choose(int32_t m, int32_t m1, int32_t m2);

@@ -76,6 +76,7 @@ SIGNATURES = {
     "fdpp_impl_c_gemm": (c_i32, [ctypes.POINTER(GemmParams), c_vp]),
     "fdpp_run_kernel": (c_i32, [c_i32, ctypes.POINTER(GemmParams), c_vp]),
     "fdpp_gemm_fused": (c_i32, [ctypes.POINTER(GemmParams), ctypes.POINTER(GemmFuse), c_vp]),
+    "fdpp_gemv_fused": (c_i32, [ctypes.POINTER(GemmParams), ctypes.POINTER(GemmFuse), c_vp]),
     "fdpp_dispatch_choose": (c_i32, [c_i32, c_i32, c_i32]),
     "fdpp_first_sustained": (c_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double), c_i32, c_i32]),
     "fdpp_profile_decide": (c_i32, [ctypes.POINTER(c_i32), ctypes.POINTER(ctypes.c_double),

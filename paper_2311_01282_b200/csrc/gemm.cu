@@ -185,6 +185,177 @@ struct GemmFuse {
     int64_t act_ld;
 };
 
+// ImplA with the decode-step fusions (M <= 2, NR = 8 rows per CTA; the ImplB
+// fusions of fdpp_gemm_fuse in GEMV form): folded-RMSNorm row scale (x_op 3),
+// residual, per-CTA sums of squares of the stored output (ssq_out: N/8 tiles),
+// RoPE + KV append for a QKV weight whose rows are permuted so each CTA holds
+// dims [4j, 4j+4) and [64+4j, 64+4j+4) of one head (the rope pairs in one CTA),
+// and SiLU*up for a gate|up weight permuted to 4 gate rows + their 4 up rows.
+template <typename T, int MR>
+__global__ void __launch_bounds__(GEMV_WARPS * 32, 2)
+gemv_fused_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W, int64_t ldw, T *C,
+                  int64_t ldc, const T *R, int64_t ldr, int M, int N, int K, const GemmFuse fz) {
+    constexpr int NR = 8;
+    constexpr int STEP = GEMV_WARPS * 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * NR;
+    const int nchunks = K >> 3;
+    __shared__ float red[GEMV_WARPS][NR][MR];
+    __shared__ float fin[NR][MR];
+    __shared__ float s_inv[MR];
+    float acc[NR][MR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int m = 0; m < MR; ++m) acc[r][m] = 0.f;
+    const T *wrow[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) wrow[r] = W + (int64_t)min(n0 + r, N - 1) * ldw;
+    // weights do not depend on the predecessor: the first chunks are requested before the wait
+    int4 wv[2][NR];
+    const int cfirst = warp * 32 + lane;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const int c = cfirst + h * STEP;
+            wv[h][r] = c < nchunks ? ld_stream_16(wrow[r] + (int64_t)c * 8) : make_int4(0, 0, 0, 0);
+        }
+    pdl_wait();
+    // folded RMSNorm: a GEMV CTA streams its token rows' whole K, so the rows'
+    // sums of squares come from the activation chunks it loads anyway (no
+    // producer-side tiles; ssq_in is not read)
+    float ssp[MR];
+#pragma unroll
+    for (int m = 0; m < MR; ++m) ssp[m] = 0.f;
+    const bool norm = fz.x_op == 3;
+    for (int c0 = cfirst; c0 < nchunks; c0 += 2 * STEP) {
+        if (c0 != cfirst) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    const int c = c0 + h * STEP;
+                    wv[h][r] = c < nchunks ? ld_stream_16(wrow[r] + (int64_t)c * 8) : make_int4(0, 0, 0, 0);
+                }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = c0 + h * STEP;
+            if (c >= nchunks) break;
+#pragma unroll
+            for (int m = 0; m < MR; ++m) {
+                const int mm = m < M ? m : M - 1;
+                int4 av = __ldg(reinterpret_cast<const int4 *>(A + (int64_t)mm * lda) + c);
+                float2 a0 = Elem<T>::to_f2(av.x), a1 = Elem<T>::to_f2(av.y);
+                float2 a2 = Elem<T>::to_f2(av.z), a3 = Elem<T>::to_f2(av.w);
+                if (norm) {
+                    float q = ssp[m];
+                    q = fmaf(a0.x, a0.x, q); q = fmaf(a0.y, a0.y, q);
+                    q = fmaf(a1.x, a1.x, q); q = fmaf(a1.y, a1.y, q);
+                    q = fmaf(a2.x, a2.x, q); q = fmaf(a2.y, a2.y, q);
+                    q = fmaf(a3.x, a3.x, q); q = fmaf(a3.y, a3.y, q);
+                    ssp[m] = q;
+                }
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    float2 w0 = Elem<T>::to_f2(wv[h][r].x), w1 = Elem<T>::to_f2(wv[h][r].y);
+                    float2 w2 = Elem<T>::to_f2(wv[h][r].z), w3 = Elem<T>::to_f2(wv[h][r].w);
+                    float s = acc[r][m];
+                    s = fmaf(a0.x, w0.x, s); s = fmaf(a0.y, w0.y, s);
+                    s = fmaf(a1.x, w1.x, s); s = fmaf(a1.y, w1.y, s);
+                    s = fmaf(a2.x, w2.x, s); s = fmaf(a2.y, w2.y, s);
+                    s = fmaf(a3.x, w3.x, s); s = fmaf(a3.y, w3.y, s);
+                    acc[r][m] = s;
+                }
+            }
+        }
+    }
+    pdl_trigger();
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int m = 0; m < MR; ++m) {
+            float v = acc[r][m];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            acc[r][m] = v;
+        }
+    __shared__ float s_ssp[GEMV_WARPS][MR];
+#pragma unroll
+    for (int m = 0; m < MR; ++m) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ssp[m] += __shfl_xor_sync(0xffffffffu, ssp[m], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int m = 0; m < MR; ++m) red[warp][r][m] = acc[r][m];
+#pragma unroll
+        for (int m = 0; m < MR; ++m) s_ssp[warp][m] = ssp[m];
+    }
+    __syncthreads();
+    if (fz.x_op == 3 && threadIdx.x < M) {  // warp order fixed
+        float ss = 0.f;
+#pragma unroll
+        for (int w = 0; w < GEMV_WARPS; ++w) ss += s_ssp[w][threadIdx.x];
+        s_inv[threadIdx.x] = rsqrtf(ss / K + fz.eps);
+    }
+    __syncthreads();
+    if (threadIdx.x < NR * MR) {  // this CTA's outputs, rounded like a stored tensor
+        const int r = threadIdx.x / MR, m = threadIdx.x % MR, n = n0 + r;
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < GEMV_WARPS; ++w) s += red[w][r][m];  // warp order fixed
+        if (fz.x_op == 3 && m < M) s *= s_inv[m];
+        if (R && n < N && m < M) s += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
+        const T h = Elem<T>::from_f(s);
+        fin[r][m] = Elem<T>::to_f(h);
+        if (!fz.q_out && !fz.act_out && n < N && m < M) C[(int64_t)m * ldc + n] = h;
+    }
+    __syncthreads();
+    if (fz.ssq_out && threadIdx.x < M) {  // tile = this CTA's NR output columns (fixed order)
+        const int m = threadIdx.x;
+        float ss = 0.f;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) ss += n0 + r < N ? fin[r][m] * fin[r][m] : 0.f;
+        fz.ssq_out[(int64_t)blockIdx.x * fz.ssq_out_ld + m] = ss;
+    }
+    if (fz.act_out && threadIdx.x < 4 * MR) {  // rows 0-3 gate, 4-7 their up rows
+        const int r = threadIdx.x / MR, m = threadIdx.x % MR;
+        if (m < M) {
+            const float g = fin[r][m], u = fin[r + 4][m];
+            static_cast<T *>(fz.act_out)[(int64_t)m * fz.act_ld + blockIdx.x * 4 + r] =
+                Elem<T>::from_f(__fdividef(g, 1.f + __expf(-g)) * u);
+        }
+    }
+    if (fz.q_out && threadIdx.x < 4 * MR) {  // rows r / r+4 = dims i / i+64 of head hd
+        const int r = threadIdx.x / MR, m = threadIdx.x % MR;
+        if (m < M) {
+            const int hd = n0 / 128, i = ((n0 % 128) / NR) * 4 + r;
+            const int p = fz.pos[m];
+            const float x0 = fin[r][m], x1 = fin[r + 4][m];
+            float lo = x0, hi = x1;
+            if (hd < fz.Hq + fz.Hkv) {
+                float sn, cs;
+                __sincosf(p * __powf(fz.theta, -2.f * i / 128), &sn, &cs);
+                lo = x0 * cs - x1 * sn;
+                hi = x1 * cs + x0 * sn;
+            }
+            T *dst = hd < fz.Hq ? static_cast<T *>(fz.q_out) + ((int64_t)m * fz.Hq + hd) * 128
+                     : hd < fz.Hq + fz.Hkv
+                         ? static_cast<T *>(fz.k_cache) + (int64_t)m * fz.cache_sb +
+                               (int64_t)(hd - fz.Hq) * fz.cache_sh + (int64_t)p * 128
+                         : static_cast<T *>(fz.v_cache) + (int64_t)m * fz.cache_sb +
+                               (int64_t)(hd - fz.Hq - fz.Hkv) * fz.cache_sh + (int64_t)p * 128;
+            dst[i] = Elem<T>::from_f(lo);
+            dst[i + 64] = Elem<T>::from_f(hi);
+        }
+    }
+}
+
+
 template <int BW, int BX, int STAGES, bool XF = false>
 struct TcSmem {
     static constexpr uint32_t W_BYTES = BW * TC_BK * 2;
@@ -837,7 +1008,6 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         pdl_wait();  // residual / C belong to earlier kernels
         const int quad = warp & 3;
         const int row = quad * 32 + lane;
-        const int n = n0 + row;
         // (s_inv_rms was filled before the accumulator wait; the cluster barrier orders it)
         // column slice of this rank: a multiple of 4 columns (16-B DSMEM loads)
         const int per = (((MMA_N + ck.cs - 1) / ck.cs) + 3) & ~3;
@@ -1345,6 +1515,67 @@ extern "C" fdpp_status fdpp_impl_b_flat(const fdpp_gemm_params *p, void *stream)
 
 extern "C" fdpp_status fdpp_impl_c_gemm(const fdpp_gemm_params *p, void *stream) {
     return run_tc(p, false, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" fdpp_status fdpp_gemv_fused(const fdpp_gemm_params *p, const fdpp_gemm_fuse *fuse, void *stream) {
+    fdpp_status s = check_gemm(p, fuse && (fuse->q_out || fuse->act_out));
+    if (s != FDPP_OK) return s;
+    FDPP_REQUIRE(fuse != nullptr, FDPP_ERR_VALUE, "null fuse descriptor");
+    FDPP_REQUIRE(p->M <= 2, FDPP_ERR_SHAPE, "fused GEMV supports M <= 2, got %d", p->M);
+    FDPP_REQUIRE(fuse->x_op == 0 || fuse->x_op == 3, FDPP_ERR_UNSUPPORTED, "fused GEMV: x_op 0 or 3");
+    FDPP_REQUIRE(!fuse->q_out || (fuse->k_cache && fuse->v_cache && fuse->pos && p->N % 128 == 0 &&
+                                  fuse->Hq + 2 * fuse->Hkv == p->N / 128),
+                 FDPP_ERR_VALUE, "RoPE epilogue needs N = (Hq + 2 Hkv) * 128 and the caches");
+    FDPP_REQUIRE(!fuse->act_out || (p->N % 8 == 0 && fuse->act_ld >= p->N / 2), FDPP_ERR_VALUE,
+                 "SiLU epilogue needs N %% 8 == 0");
+    FDPP_REQUIRE((reinterpret_cast<uintptr_t>(p->a) & 15) == 0 && (reinterpret_cast<uintptr_t>(p->w) & 15) == 0,
+                 FDPP_ERR_UNSUPPORTED, "GEMV operands must be 16-byte aligned");
+    GemmFuse fz;
+    memset(&fz, 0, sizeof(fz));
+    fz.x_op = fuse->x_op;
+    fz.ssq_in = fuse->ssq_in;
+    fz.ssq_tiles = fuse->ssq_tiles;
+    fz.ssq_ld = fuse->ssq_ld;
+    fz.eps = fuse->eps;
+    fz.ssq_out = fuse->ssq_out;
+    fz.ssq_out_ld = fuse->ssq_out_ld;
+    fz.q_out = fuse->q_out;
+    fz.k_cache = fuse->k_cache;
+    fz.v_cache = fuse->v_cache;
+    fz.pos = fuse->pos;
+    fz.Hq = fuse->Hq;
+    fz.Hkv = fuse->Hkv;
+    fz.cache_sb = fuse->cache_stride_b;
+    fz.cache_sh = fuse->cache_stride_h;
+    fz.theta = fuse->theta;
+    fz.act_out = fuse->act_out;
+    fz.act_ld = fuse->act_ld;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    dim3 grid(ceil_div(p->N, 8));
+    cudaError_t e;
+    if (p->dtype == FDPP_BF16) {
+        using T = __nv_bfloat16;
+        e = p->M == 1 ? launch_kernel(gemv_fused_kernel<T, 1>, grid, dim3(GEMV_WARPS * 32), 0, st,
+                                      static_cast<const T *>(p->a), p->lda, static_cast<const T *>(p->w), p->ldw,
+                                      static_cast<T *>(p->c), p->ldc, static_cast<const T *>(p->r), p->ldr,
+                                      p->M, p->N, p->K, fz)
+                      : launch_kernel(gemv_fused_kernel<T, 2>, grid, dim3(GEMV_WARPS * 32), 0, st,
+                                      static_cast<const T *>(p->a), p->lda, static_cast<const T *>(p->w), p->ldw,
+                                      static_cast<T *>(p->c), p->ldc, static_cast<const T *>(p->r), p->ldr,
+                                      p->M, p->N, p->K, fz);
+    } else {
+        using T = __half;
+        e = p->M == 1 ? launch_kernel(gemv_fused_kernel<T, 1>, grid, dim3(GEMV_WARPS * 32), 0, st,
+                                      static_cast<const T *>(p->a), p->lda, static_cast<const T *>(p->w), p->ldw,
+                                      static_cast<T *>(p->c), p->ldc, static_cast<const T *>(p->r), p->ldr,
+                                      p->M, p->N, p->K, fz)
+                      : launch_kernel(gemv_fused_kernel<T, 2>, grid, dim3(GEMV_WARPS * 32), 0, st,
+                                      static_cast<const T *>(p->a), p->lda, static_cast<const T *>(p->w), p->ldw,
+                                      static_cast<T *>(p->c), p->ldc, static_cast<const T *>(p->r), p->ldr,
+                                      p->M, p->N, p->K, fz);
+    }
+    if (e != cudaSuccess) return cuda_status(e, "gemv_fused_kernel launch");
+    return FDPP_OK;
 }
 
 extern "C" fdpp_status fdpp_gemm_fused(const fdpp_gemm_params *p, const fdpp_gemm_fuse *fuse,

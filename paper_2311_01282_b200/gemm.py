@@ -176,9 +176,33 @@ def interleave_gate_up(pw: PackedWeight) -> PackedWeight:
     return PackedWeight(pw.w[idx].contiguous(), pw.K, pw.N)
 
 
+def permute_qkv_for_gemv(pw: PackedWeight) -> PackedWeight:
+    """QKV rows per 128-row head reordered to [4j..4j+3, 64+4j..64+4j+3] per
+    8-row block: each fused-GEMV CTA holds the RoPE pairs (i, i+64)."""
+    torch = _torch()
+    if pw.N % 128:
+        raise ShapeError("QKV width must be (Hq + 2 Hkv) * 128")
+    j = torch.arange(16, device=pw.w.device)[:, None] * 4 + torch.arange(4, device=pw.w.device)[None, :]
+    head = torch.cat([j, j + 64], 1).reshape(-1)                       # 128 within-head rows
+    idx = (torch.arange(pw.N // 128, device=pw.w.device)[:, None] * 128 + head[None, :]).reshape(-1)
+    return PackedWeight(pw.w[idx].contiguous(), pw.K, pw.N)
+
+
+def permute_gate_up_for_gemv(pw: PackedWeight) -> PackedWeight:
+    """[gate; up] rows reordered to [gate 4c..4c+3, up 4c..4c+3] per 8-row block
+    (the fused GEMV's SiLU*up epilogue)."""
+    torch = _torch()
+    F = pw.N // 2
+    if F % 4:
+        raise ShapeError("gate|up width must be a multiple of 8")
+    c = torch.arange(F // 4, device=pw.w.device)[:, None] * 4 + torch.arange(4, device=pw.w.device)[None, :]
+    idx = torch.cat([c, c + F], 1).reshape(-1)
+    return PackedWeight(pw.w[idx].contiguous(), pw.K, pw.N)
+
+
 def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ssq_in=None,
               ssq_tiles: int = 0, norm_w=None, eps: float = 1e-5, ssq_out=None, rope=None,
-              silu_out=None, stream=None, ws_tag="gemm"):
+              silu_out=None, impl: str = "B", stream=None, ws_tag="gemm"):
     """ImplB with the decode-step fusions (fdpp_gemm_fused).
 
     x_op 1: the activation tile is RMSNorm(a) * norm_w, with the rows' sums of
@@ -188,7 +212,9 @@ def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ss
     output rows (for the next GEMM's x_op 1).  rope = dict(q_out, k_cache,
     v_cache, pos, theta): RoPE the q/k heads and append k/v at row pos[m]
     (QKV projection; ``out`` unused).  silu_out [M, N/2]: silu(gate) * up of a
-    tile-interleaved gate|up weight (interleave_gate_up; ``out`` unused)."""
+    tile-interleaved gate|up weight (interleave_gate_up; ``out`` unused).
+    impl "A": the GEMV form (fdpp_gemv_fused, M <= 2, x_op 0/3): ssq_out has
+    N/8 tiles, rope / silu_out need the permute_*_for_gemv weight layouts."""
     torch = _torch()
     K = pw.ldw
     if x_op == 2:
@@ -227,6 +253,10 @@ def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ss
     if silu_out is not None:
         fz.act_out, fz.act_ld = silu_out.data_ptr(), silu_out.stride(0)
     lib = _lib.load()
+    if impl == "A":
+        _lib.check(lib.fdpp_gemv_fused(ctypes.byref(prm), ctypes.byref(fz), _lib.stream_handle(stream)),
+                   "gemv_fused")
+        return out
     need = ctypes.c_size_t()
     _lib.check(lib.fdpp_gemm_workspace_size(IMPL_B, ctypes.byref(prm), ctypes.byref(need)), "gemm_fused")
     if need.value:

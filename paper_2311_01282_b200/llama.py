@@ -30,7 +30,8 @@ import torch
 from . import _lib, tp as _tp, workspace
 from . import dispatch as _dispatch_mod  # noqa: F401  (module, not the function)
 from .attention import AttentionConfig, decode_attention
-from .gemm import PackedWeight, interleave_gate_up, run_fused
+from .gemm import (PackedWeight, interleave_gate_up, permute_gate_up_for_gemv, permute_qkv_for_gemv,
+                   run_fused)
 from .softmax import ScalingCalibration
 
 import importlib
@@ -102,7 +103,7 @@ class LlamaDecoder:
                  calib: ScalingCalibration = GOLDEN_CALIB, dtype=torch.float16, seed: int = 0,
                  attn_p: int = 0, attn_splits: int = 0, n_layers: int = None, fused: bool = True,
                  tp_rank: int = 0, tp_size: int = 1, group=None, weights: dict = None,
-                 collective: bool = True):
+                 collective: bool = True, gemv_step: bool = False):
         """tp_size > 1: this process is rank tp_rank of a tensor-parallel group
         (tp.py): sharded QKV / O / gate|up / down, local heads and KV cache, one
         NCCL all-reduce of the residual stream after O and after down (captured
@@ -178,8 +179,10 @@ class LlamaDecoder:
         # GEMM's RMSNorm prologue
         self.fused = fused
         nt = max(1, -(-cfg.hidden // 128))
-        self.ssq_a = torch.zeros((nt, B), dtype=torch.float32, device=dev)
-        self.ssq_b = torch.zeros((nt, B), dtype=torch.float32, device=dev)
+        # sized for either producer: ImplB epilogues write hidden/128 tiles, the
+        # fused GEMV one tile per 8 columns
+        self.ssq_a = torch.zeros((max(nt, cfg.hidden // 8), B), dtype=torch.float32, device=dev)
+        self.ssq_b = torch.zeros_like(self.ssq_a)
         self.ssq_tiles = nt
         self.recomputed = torch.zeros(1, dtype=torch.int32, device=dev)
         self.attn_cfg = AttentionConfig(p=attn_p, scale=1.0 / math.sqrt(Dh), calib=calib,
@@ -196,15 +199,27 @@ class LlamaDecoder:
         # is slower (profiles/r1_bench: 3.33 vs 2.80 ms).  ImplC (M beyond the
         # flat-GEMM band) still forces the unfused step.
         fused = fused and all(c != D.KernelChoice.IMPL_C for c in self.table_choices.values())
-        self.choices = ({op: D.KernelChoice.IMPL_B for op in shapes} if fused else dict(self.table_choices))
+        # gemv_step (B <= 2, the table picking the GEMV for every projection): the
+        # fused step on fdpp_gemv_fused.  Off by default: per GEMM it ties ImplB and
+        # the B = 1 step measured 2.93 vs 2.83 ms on ImplB (the GEMV epilogues' scattered
+        # RoPE / SiLU stores; profiles/r1_bench).
+        self.step_impl = ("A" if gemv_step and fused and B <= 2 and all(
+            c == D.KernelChoice.IMPL_A for c in self.table_choices.values()) else "B")
+        self.gemv_ssq_tiles = cfg.hidden // 8
+        kind = D.KernelChoice.IMPL_A if self.step_impl == "A" else D.KernelChoice.IMPL_B
+        self.choices = ({op: kind for op in shapes} if fused else dict(self.table_choices))
         if tp_size > 1 and not fused:
             raise NotImplementedError("tensor parallelism runs on the fused (ImplB) decode step")
         self.graph = None
         self._layer_hook = None  # calibrate(): samples attention inputs after each QKV
         if fused:  # fold the RMSNorm weights into the following projections' columns
             for L in self.layers:
-                L["qkv_f"] = fold_norm(L["qkv"], L["ln1"])
-                L["gate_up_f"] = interleave_gate_up(fold_norm(L.pop("gate_up"), L["ln2"]))
+                if self.step_impl == "A":
+                    L["qkv_f"] = permute_qkv_for_gemv(fold_norm(L["qkv"], L["ln1"]))
+                    L["gate_up_f"] = permute_gate_up_for_gemv(fold_norm(L.pop("gate_up"), L["ln2"]))
+                else:
+                    L["qkv_f"] = fold_norm(L["qkv"], L["ln1"])
+                    L["gate_up_f"] = interleave_gate_up(fold_norm(L.pop("gate_up"), L["ln2"]))
             self.lm_head_f = fold_norm(self.lm_head, self.ln_f)
         self.fused = fused
         # fused: embed + L x (qkv+rope, attn async, attn recompute, o, gate_up+silu, down
@@ -281,6 +296,9 @@ class LlamaDecoder:
         Hq, Dh = self.n_heads_local, cfg.head_dim
         tp = self.tp_size > 1
         lead = self.tp_rank == 0  # the rank whose row-parallel epilogue adds the residual
+        impl = self.step_impl      # "B": tcgen05 flat GEMM; "A": fused GEMV (B <= 2)
+        # sums-of-squares tiles the residual GEMMs leave for the next folded RMSNorm
+        res_tiles = 1 if tp else (self.gemv_ssq_tiles if impl == "A" else self.ssq_tiles)
 
         def all_reduce_x(ssq):
             # x = sum over ranks of (x + partial_0, partial_1, ...); then the
@@ -297,7 +315,7 @@ class LlamaDecoder:
         for li, L in enumerate(self.layers):
             kc, vc = self.k_cache[li], self.v_cache[li]
             run_fused(self.x, L["qkv_f"], x_op=3, ssq_in=self.ssq_a, ssq_tiles=ssq_tiles,
-                      eps=cfg.eps, ws_tag="decode_gemm",
+                      eps=cfg.eps, ws_tag="decode_gemm", impl=impl,
                       rope={"q_out": self.q, "k_cache": kc, "v_cache": vc, "pos": self.pos,
                             "theta": cfg.rope_theta})
             if self._layer_hook is not None:
@@ -305,18 +323,18 @@ class LlamaDecoder:
             decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
                              seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed)
             run_fused(self.attn.view(B, Hq * Dh), L["o"], out=self.x, residual=self.x if lead else None,
-                      ssq_out=None if tp else self.ssq_b, ws_tag="decode_gemm")
+                      ssq_out=None if tp or impl == "A" else self.ssq_b, ws_tag="decode_gemm", impl=impl)
             if tp:
-                all_reduce_x(self.ssq_b)
+                all_reduce_x(self.ssq_b)  # (the fused GEMV re-derives the norm from x itself)
             run_fused(self.x, L["gate_up_f"], x_op=3, ssq_in=self.ssq_b, silu_out=self.act,
-                      ssq_tiles=1 if tp else self.ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
+                      ssq_tiles=res_tiles, eps=cfg.eps, ws_tag="decode_gemm", impl=impl)
             run_fused(self.act, L["down"], out=self.x, residual=self.x if lead else None,
-                      ssq_out=None if tp else self.ssq_a, ws_tag="decode_gemm")
+                      ssq_out=None if tp or impl == "A" else self.ssq_a, ws_tag="decode_gemm", impl=impl)
             if tp:
                 all_reduce_x(self.ssq_a)
-            ssq_tiles = 1 if tp else self.ssq_tiles
+            ssq_tiles = res_tiles
         run_fused(self.x, self.lm_head_f, out=self.logits, x_op=3, ssq_in=self.ssq_a,
-                  ssq_tiles=ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm")
+                  ssq_tiles=ssq_tiles, eps=cfg.eps, ws_tag="decode_gemm", impl=impl)
         _lib.check(lib.fdpp_argmax(self.logits.data_ptr(), self.ids.data_ptr(), B, cfg.vocab, dt, st),
                    "argmax")
         _lib.check(lib.fdpp_advance_positions(self.pos.data_ptr(), self.lens.data_ptr(), B, st),

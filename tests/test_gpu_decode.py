@@ -156,8 +156,8 @@ def _tiny_weights(torch, cfg, seed=0):
             "lm_head": w(cfg.vocab, cfg.hidden), "ln_f": 1 + 0.1 * torch.randn(cfg.hidden, generator=g)}
 
 
-@pytest.mark.parametrize("n_kv", [4, 1])  # MHA-style CUDA-core attention; G = 8 tensor-core attention
-def test_decode_step_matches_fp32_reference(torch, mods, n_kv):
+@pytest.mark.parametrize("n_kv,B,m1", [(4, 4, 1), (1, 4, 1), (4, 2, 3)])  # ImplB step; G = 8; fused GEMV step
+def test_decode_step_matches_fp32_reference(torch, mods, n_kv, B, m1):
     """The whole fused decode step (folded RMSNorm, RoPE + KV append epilogue,
     async attention, residual epilogues, SiLU*up) against tp.reference_layer
     in fp32 on the same weights, KV state and tokens."""
@@ -168,10 +168,10 @@ def test_decode_step_matches_fp32_reference(torch, mods, n_kv):
     W = _tiny_weights(torch, cfg)
     table = D.DispatchTable(fingerprint="test")
     for n, k in cfg.gemm_shapes().values():
-        table.add(D.DispatchEntry(n=n, k=k, m1=1, m2=128))
-    B, L = 4, 200
-    dec = llama.LlamaDecoder(cfg, B, L + 8, table=table, weights=W)
-    assert dec.fused
+        table.add(D.DispatchEntry(n=n, k=k, m1=m1, m2=128))
+    L = 200
+    dec = llama.LlamaDecoder(cfg, B, L + 8, table=table, weights=W, gemv_step=m1 > B)
+    assert dec.fused and dec.step_impl == ("A" if m1 > B else "B")
     dec.prefill_random(L, seed=3)
     x = W["embed"][dec.ids.long().cpu()].half().float()
     kc = [k.float().cpu() for k in dec.k_cache]
@@ -231,3 +231,55 @@ def test_decoder_calibrate(torch, mods):
     dec.enqueue_step()
     torch.cuda.synchronize()
     assert int(dec.recomputed.item()) == 0
+
+
+@pytest.mark.parametrize("M", [1, 2])
+def test_fused_gemv_matches_fused_flat_gemm(torch, mods, M):
+    """fdpp_gemv_fused (ImplA form of the decode-step fusions) against the
+    ImplB fused GEMM: residual + sums of squares, folded RMSNorm, RoPE + KV
+    append (permuted QKV rows), SiLU*up (permuted gate|up rows)."""
+    fd, _lib, gemm, _, D = mods
+    g = torch.Generator(device="cuda").manual_seed(M)
+    H = 1024
+    x = torch.randn((M, H), generator=g, device="cuda").half()
+    res = torch.randn((M, H), generator=g, device="cuda").half()
+    ssq_in = (x.float() ** 2).sum(1, keepdim=True).t().contiguous()      # one tile per row
+    # residual GEMM with sums of squares
+    w = fd.PackedWeight((torch.randn((H, H), generator=g, device="cuda") / 32).half(), H, H)
+    o_b, o_a = torch.empty_like(res), torch.empty_like(res)
+    s_b = torch.zeros((H // 128, M), device="cuda")
+    s_a = torch.zeros((H // 8, M), device="cuda")
+    gemm.run_fused(x, w, out=o_b, residual=res, ssq_out=s_b)
+    gemm.run_fused(x, w, out=o_a, residual=res, ssq_out=s_a, impl="A")
+    torch.cuda.synchronize()
+    assert _rel(o_a, o_b) <= 2e-3
+    assert torch.allclose(s_a.sum(0), s_b.sum(0), rtol=1e-3)
+    # folded RMSNorm
+    f_b = gemm.run_fused(x, w, x_op=3, ssq_in=ssq_in, ssq_tiles=1)
+    f_a = gemm.run_fused(x, w, x_op=3, ssq_in=ssq_in, ssq_tiles=1, impl="A")
+    torch.cuda.synchronize()
+    assert _rel(f_a, f_b) <= 2e-3
+    # RoPE + KV append
+    Hq, Hkv, Lmax = 4, 2, 16
+    wq = fd.PackedWeight((torch.randn(((Hq + 2 * Hkv) * 128, H), generator=g, device="cuda") / 32).half(),
+                         H, (Hq + 2 * Hkv) * 128)
+    pos = torch.tensor([3, 9][:M], dtype=torch.int32, device="cuda")
+    outs = []
+    for impl, ww in (("B", wq), ("A", gemm.permute_qkv_for_gemv(wq))):
+        q = torch.zeros((M, Hq, 128), device="cuda").half()
+        kc = torch.zeros((M, Hkv, Lmax, 128), device="cuda").half()
+        vc = torch.zeros_like(kc)
+        gemm.run_fused(x, ww, rope={"q_out": q, "k_cache": kc, "v_cache": vc, "pos": pos}, impl=impl)
+        outs.append((q, kc, vc))
+    torch.cuda.synchronize()
+    for a, b in zip(outs[0], outs[1]):
+        assert _rel(b.reshape(M, -1), a.reshape(M, -1)) <= 2e-3
+    # SiLU*up
+    F = 768
+    wg = fd.PackedWeight((torch.randn((2 * F, H), generator=g, device="cuda") / 32).half(), H, 2 * F)
+    act_b = torch.empty((M, F), device="cuda").half()
+    act_a = torch.empty_like(act_b)
+    gemm.run_fused(x, gemm.interleave_gate_up(wg), silu_out=act_b)
+    gemm.run_fused(x, gemm.permute_gate_up_for_gemv(wg), silu_out=act_a, impl="A")
+    torch.cuda.synchronize()
+    assert _rel(act_a, act_b) <= 2e-3
