@@ -233,6 +233,22 @@ fdpp_status fdpp_row_ssq(const void *x, float *ssq_out, int32_t B, int32_t dim, 
  * The host fits phi and the band with calibrate() (softmax.py:219-266). */
 fdpp_status fdpp_sample_logits(const fdpp_attn_params *p, int32_t n, uint64_t seed, float *out,
                                int32_t *idx_out, void *stream);
+
+/* ---------------------------------------------- vector softmax APIs (rows a5/a6) */
+/* softmax_reference[_f64] (softmax.py:90-100): exp(x - max) / sum in f64; f64 = 0: f32 x and
+ * out (softmax_reference), f64 = 1: f64 x and out (softmax_reference_f64). */
+fdpp_status fdpp_softmax_reference(const void *x, int32_t n, void *out, int32_t f64, void *stream);
+/* softmax_unified (softmax.py:146-172): e = expf(x - phi), f64 sum.  status[0] = first
+ * non-finite e index (INT_MAX if none), *total = the f64 sum; out is written only when
+ * the result is representable (the host raises SoftmaxOverflow / DegenerateSumError). */
+fdpp_status fdpp_softmax_unified(const float *x, int32_t n, float phi, float *out, int32_t *status,
+                                 double *total, void *stream);
+/* error path: status[1] = first index where the running f64 sum exceeds FLT_MAX. */
+fdpp_status fdpp_softmax_overflow_index(const float *x, int32_t n, float phi, int32_t *status, void *stream);
+/* partial_softmax_sync (softmax.py:113-143) over chunk bounds[p+1] (chunk_bounds):
+ * per-chunk (max, f32 exp-sum) into ml[2p], merged in chunk order, rescaled output. */
+fdpp_status fdpp_partial_softmax_sync(const float *x, const int64_t *bounds, int32_t p, float *out, float *ml,
+                                      void *stream);
 /* ids[r] = argmax_j logits[r, j] (lowest index on ties). */
 fdpp_status fdpp_argmax(const void *logits, int32_t *ids, int32_t rows, int32_t vocab,
                         int32_t dtype, void *stream);

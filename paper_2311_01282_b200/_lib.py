@@ -90,6 +90,10 @@ SIGNATURES = {
     "fdpp_embed": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_vp, c_i32, c_vp]),
     "fdpp_row_ssq": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_sample_logits": (c_i32, [ctypes.POINTER(AttnParams), c_i32, ctypes.c_uint64, c_vp, c_vp, c_vp]),
+    "fdpp_softmax_reference": (c_i32, [c_vp, c_i32, c_vp, c_i32, c_vp]),
+    "fdpp_softmax_unified": (c_i32, [c_vp, c_i32, c_f32, c_vp, c_vp, c_vp, c_vp]),
+    "fdpp_softmax_overflow_index": (c_i32, [c_vp, c_i32, c_f32, c_vp, c_vp]),
+    "fdpp_partial_softmax_sync": (c_i32, [c_vp, c_vp, c_i32, c_vp, c_vp, c_vp]),
     "fdpp_argmax": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "fdpp_advance_positions": (c_i32, [c_vp, c_vp, c_i32, c_vp]),
 }

@@ -233,3 +233,31 @@ def test_sample_logits_and_calibrate(fd, torch):
     cal = fd.calibrate(s.cpu().numpy(), 0.9999, 1.0)
     x = s.cpu().numpy() - cal.phi
     assert ((x > cal.a) & (x < cal.b)).mean() >= 0.9999
+
+
+def test_vector_softmax_apis_match_golden(fd):
+    """softmax_reference / softmax_unified / partial_softmax_sync (SURVEY §8a rows
+    a5/a6) on the device against the real reference's golden vectors."""
+    import os
+    S = np.load(os.path.join(os.path.dirname(__file__), "golden", "softmax.npz"))
+    for i in range(int(S["n_cases"])):
+        x = S[f"s{i}_x"]
+        assert fd.rel_error_elementwise(fd.softmax_reference(x), S[f"s{i}_ref"]) <= 2e-6
+        assert fd.rel_error_elementwise(fd.softmax_unified(x, 0.0), S[f"s{i}_unified_phi0"]) <= 2e-6
+        assert fd.rel_error_elementwise(fd.softmax_unified(x, 6.0), S[f"s{i}_unified_phi6"]) <= 2e-6
+        for p in (1, 2, 4):
+            if p <= x.size:
+                assert fd.rel_error_elementwise(fd.partial_softmax_sync(x, p), S[f"s{i}_sync_p{p}"]) <= 2e-5
+        ref64 = fd.softmax_reference_f64(x.astype(np.float64))
+        assert ref64.dtype == np.float64 and abs(ref64.sum() - 1.0) < 1e-12
+    a = fd.softmax_unified(np.zeros(5, np.float32), 0.0)
+    assert np.allclose(a, 0.2)
+    with pytest.raises(fd.SoftmaxOverflow) as e:
+        fd.softmax_unified(np.array([0.0, 100.0, 1.0], np.float32), 0.0)   # e^100 overflows f32
+    assert e.value.index == 1
+    with pytest.raises(fd.DegenerateSumError):
+        fd.softmax_unified(np.array([-200.0, -300.0], np.float32), 0.0)    # all underflow
+    with pytest.raises(ValueError):
+        fd.softmax_unified(np.array([np.nan], np.float32), 0.0)
+    with pytest.raises(ValueError):
+        fd.partial_softmax_sync(np.ones(3, np.float32), 4)                  # p > n
