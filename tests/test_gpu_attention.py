@@ -261,3 +261,23 @@ def test_vector_softmax_apis_match_golden(fd):
         fd.softmax_unified(np.array([np.nan], np.float32), 0.0)
     with pytest.raises(ValueError):
         fd.partial_softmax_sync(np.ones(3, np.float32), 4)                  # p > n
+
+
+@pytest.mark.parametrize("Hkv", [8, 1])  # MHA (CUDA cores) and G = 8 (tensor cores)
+@pytest.mark.parametrize("p", [0, 3])
+def test_ragged_seq_lens(fd, torch, Hkv, p):
+    """Per-row attended lengths on the device (the decode step's seq_lens):
+    ragged rows, a 1-key row, rows shorter than the chunk count."""
+    B, Hq, L, D = 4, 8, 300, 128
+    q, k, v = _qkv(torch, B, Hq, Hkv, L, D, 21 + Hkv, torch.float16)
+    lens = torch.tensor([300, 1, 77, 129], dtype=torch.int32, device="cuda")
+    calib = fd.ScalingCalibration(*GOLD_CAL, coverage=1.0)
+    cfg = fd.AttentionConfig(p=p, scale=1 / math.sqrt(D), calib=calib)
+    o, st = fd.decode_attention(q, k, v, cfg, "async", seq_lens=lens)
+    G = Hq // Hkv
+    qn, kn, vn = (t.float().cpu().numpy() for t in (q, k, v))
+    for b, n in enumerate(lens.tolist()):
+        for h in range(Hq):
+            ref = O.attention_reference(qn[b, h][None], kn[b, h // G, :n], vn[b, h // G, :n], cfg.scale)
+            assert fd.rel_error_rowwise(o[b, h][None].float().cpu().numpy(), ref) <= TOL
+    assert st.rows_recomputed == 0
