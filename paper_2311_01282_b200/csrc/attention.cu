@@ -910,6 +910,10 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
         if (args.list_mode) {
             pdl_wait();  // the list comes from the async launch
             const int count = __ldcg(args.flag_count);
+            if (count == 0) {  // nothing flagged (the common case): no list to walk or clear
+                pdl_trigger();
+                return;
+            }
             const int P = args.p * args.nsub;
             const int64_t items = (int64_t)count * args.n_rg * P;
             for (int64_t i = blockIdx.x; i < items; i += gridDim.x) {
