@@ -284,6 +284,13 @@ def run_gpu(args):
             for r in range(args.inject):
                 b, h = r % B, (r // B) % dec.n_kv_heads_local
                 kc[b, h, L // 2].mul_(40.0)
+    cal = None
+    if args.calibrate:
+        # fit phi / the band to this model's own logits (device-sampled after every
+        # layer's QKV, then the reference's calibrate).  Off by default: at
+        # coverage 0.9999 of single logits ~10% of 1K-key rows hold one outlier
+        # and recompute (measured 9593 vs 3071 recomputed rows, 6.16 vs 5.97 ms)
+        cal = dec.calibrate(target_coverage=args.calibrate, margin=1.0, samples_per_layer=32768)
     dec.capture()
     for _ in range(W):
         dec.step()
@@ -433,7 +440,11 @@ def run_gpu(args):
                                 + (", GQA/MQA on tensor cores" if cfg.n_heads // cfg.n_kv_heads >= 4 else ""),
                    "gemm_choices": {op: c.value for op, c in dec.choices.items()},
                    "dispatch_table_choices": {op: c.value for op, c in dec.table_choices.items()},
-                   "injected_groups_per_layer": args.inject},
+                   "injected_groups_per_layer": args.inject,
+                   "calibration": ("golden (SURVEY a1)" if cal is None else
+                                   {"phi": round(cal.phi, 4), "a": round(cal.a, 4), "b": round(cal.b, 4),
+                                    "coverage": round(cal.coverage, 6),
+                                    "source": "LlamaDecoder.calibrate on this model's logits"})},
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": B * 4,
                 "d2h_bytes_per_step": B * 4},
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(dom["gbs"], 1),
@@ -511,6 +522,8 @@ def main():
     ap.add_argument("--tp", type=int, default=1, help="tensor-parallel ranks per replica (torchrun)")
     ap.add_argument("--tp-shard", type=int, default=1,
                     help="single GPU: run rank 0's shard of a T-way TP step (all-reduce omitted)")
+    ap.add_argument("--calibrate", type=float, default=0.0,
+                    help="calibrate phi/band on the model's logits at this coverage (default: SURVEY a1's golden calibration)")
     ap.add_argument("--inject", type=int, default=0,
                     help="(batch, kv-head) groups per layer forced through the recompute path")
     args = ap.parse_args()
