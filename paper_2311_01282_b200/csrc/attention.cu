@@ -1037,11 +1037,24 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
         int maxs = per_chunk / 128 > 0 ? per_chunk / 128 : 1;
         lay->nsub = want < 1 ? 1 : (want > maxs ? maxs : want);
     }
-    if (p->p <= 0 && p->splits_per_chunk <= 0 && !lay->mma && lay->p * lay->nsub <= 16 &&
-        lay->p * lay->nsub <= p->L) {
-        // auto, CUDA-core path: make each CTA one semantic chunk, so the <= 16 CTAs of a
-        // row group can join over DSMEM as one cluster
-        lay->p *= lay->nsub;
+    if (p->p <= 0 && p->splits_per_chunk <= 0 && !lay->mma) {
+        // auto, CUDA-core path: one semantic chunk per CTA (the <= 16 CTAs of a row
+        // group join over DSMEM as one cluster).  p0 = the fewest chunks filling half
+        // a wave of the 3-per-SM slots (W = CTAs / slots >= 0.5); p0 + 1 only if it
+        // fills its last wave better (W / ceil(W); W <= 1 counts as W), >= 128 keys
+        // per CTA.  Measured (profiles/r1_attn_mha_splits.txt): B=1: 8, B=4: 3,
+        // B=8: 1 (2 = 1.15 waves is the worst), B=16: 2, B=32: 2, B=64: 1.
+        const double slots = 3.0 * sms;
+        int pmax = p->L / 128 > 0 ? p->L / 128 : 1;
+        if (pmax > 16) pmax = 16;
+        auto fill = [&](int c) {
+            const double w = (double)groups * c / slots;
+            return w <= 1.0 ? w : w / std::ceil(w);
+        };
+        int p0 = 1;
+        while (p0 < pmax && (double)groups * p0 / slots < 0.5) ++p0;
+        const int best = (p0 < pmax && fill(p0 + 1) > fill(p0) + 1e-9) ? p0 + 1 : p0;
+        lay->p = best;
         lay->nsub = 1;
     }
     lay->P = lay->p * lay->nsub;
