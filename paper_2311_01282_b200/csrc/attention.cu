@@ -1042,7 +1042,7 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
         // group join over DSMEM as one cluster).  p0 = the fewest chunks filling half
         // a wave of the 3-per-SM slots (W = CTAs / slots >= 0.5); p0 + 1 only if it
         // fills its last wave better (W / ceil(W); W <= 1 counts as W), >= 128 keys
-        // per CTA.  Measured (profiles/r1_attn_mha_splits.txt): B=1: 8, B=4: 3,
+        // per CTA.  Measured (profiles/r1_attn_mha_splits.txt, L ~ 1K): B=1: 8, B=4: 3,
         // B=8: 1 (2 = 1.15 waves is the worst), B=16: 2, B=32: 2, B=64: 1.
         const double slots = 3.0 * sms;
         int pmax = p->L / 128 > 0 ? p->L / 128 : 1;
@@ -1053,7 +1053,12 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
         };
         int p0 = 1;
         while (p0 < pmax && (double)groups * p0 / slots < 0.5) ++p0;
-        const int best = (p0 < pmax && fill(p0 + 1) > fill(p0) + 1e-9) ? p0 + 1 : p0;
+        // long rows with few row groups amortise the per-CTA cost: look two chunk
+        // counts further (B=8/16, L=8K: p=3; B=32/64, L=4K keep 2/1)
+        const int span = (p->L > 2048 && (double)groups * p0 / slots < 2.0) ? 2 : 1;
+        int best = p0;
+        for (int c = p0 + 1; c <= p0 + span && c <= pmax; ++c)
+            if (fill(c) > fill(best) + 1e-9) best = c;
         lay->p = best;
         lay->nsub = 1;
     }
