@@ -87,6 +87,18 @@ inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, 
 fdpp_status make_kmajor_map(CUtensorMap *out, const void *ptr, int64_t rows, int64_t cols, int64_t ld,
                             int box_rows, int dtype);
 
+// RoPE angle p * theta^(-2i/D) in double, reduced to [-pi, pi], then the fast
+// intrinsic: accurate at 32K-scale positions (a float angle alone is off by up
+// to ~2e-3 rad there, and __sincosf's own reduction degrades with |x|)
+__device__ __forceinline__ double rope_inv_freq(float theta, int i, int D) {
+    return pow((double)theta, -2.0 * i / D);
+}
+__device__ __forceinline__ void rope_sincos(int p, double inv_freq, float *sn, float *cs) {
+    const double x = (double)p * inv_freq;
+    const double r = x - rint(x * 0.15915494309189535) * 6.283185307179586;
+    __sincosf((float)r, sn, cs);
+}
+
 // ------------------------------------------------------------- element types
 template <typename T> struct Elem;
 template <> struct Elem<__half> {

@@ -47,9 +47,9 @@ __global__ void rope_append_kernel(const T *__restrict__ qkv, T *__restrict__ q_
     const int p = pos[b];
     for (int idx = threadIdx.x; idx < (Hq + Hkv) * half; idx += blockDim.x) {
         const int h = idx / half, i = idx % half;
-        const float inv_freq = __powf(theta, -2.f * i / D);
+        const double inv_freq = rope_inv_freq(theta, i, D);
         float sn, cs;
-        __sincosf(p * inv_freq, &sn, &cs);
+        rope_sincos(p, inv_freq, &sn, &cs);
         const T *src = row + h * D;  // q heads then k heads are contiguous in the fused row
         const float x0 = Elem<T>::to_f(src[i]), x1 = Elem<T>::to_f(src[i + half]);
         const T r0 = Elem<T>::from_f(x0 * cs - x1 * sn), r1 = Elem<T>::from_f(x1 * cs + x0 * sn);

@@ -339,7 +339,7 @@ gemv_fused_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W,
             float lo = x0, hi = x1;
             if (hd < fz.Hq + fz.Hkv) {
                 float sn, cs;
-                __sincosf(p * __powf(fz.theta, -2.f * i / 128), &sn, &cs);
+                rope_sincos(p, rope_inv_freq(fz.theta, i, 128), &sn, &cs);
                 lo = x0 * cs - x1 * sn;
                 hi = x1 * cs + x0 * sn;
             }
@@ -1042,7 +1042,7 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         if (rope) {
             // tile tn is one head: q heads [0, Hq), k heads [Hq, Hq+Hkv), v heads after
             const int i = row & 63;
-            const float inv_freq = __powf(fz.theta, -2.f * i / 128);
+            const double inv_freq = rope_inv_freq(fz.theta, i, 128);
             for (int c = c_beg; c < c_end; ++c) {
                 const int m = m0 + c;
                 if (m >= M) continue;
@@ -1052,7 +1052,7 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
                 float val;
                 if (tn < fz.Hq + fz.Hkv) {
                     float sn, cs;
-                    __sincosf(p * inv_freq, &sn, &cs);
+                    rope_sincos(p, inv_freq, &sn, &cs);
                     const float x0 = xr[i], x1 = xr[i + 64];
                     val = row < 64 ? x0 * cs - x1 * sn : x1 * cs + x0 * sn;
                     dst = tn < fz.Hq

@@ -284,3 +284,28 @@ def test_fused_gemv_matches_fused_flat_gemm(torch, mods, M):
     gemm.run_fused(x, gemm.permute_gate_up_for_gemv(wg), silu_out=act_a, impl="A")
     torch.cuda.synchronize()
     assert _rel(act_a, act_b) <= 2e-3
+
+
+def test_rope_epilogue_long_positions(torch, mods):
+    """RoPE + KV append at 32K-scale positions (ChatGLM2 config: L = 32K) against
+    an f64-angle rotation of the plain projection (full-range sin/cos)."""
+    from paper_2311_01282_b200 import tp
+    fd, _lib, gemm, _, D = mods
+    g = torch.Generator(device="cuda").manual_seed(9)
+    M, H, Hq, Hkv = 2, 1024, 2, 1
+    N = (Hq + 2 * Hkv) * 128
+    x = torch.randn((M, H), generator=g, device="cuda").half()
+    w = fd.PackedWeight((torch.randn((N, H), generator=g, device="cuda") / 32).half(), H, N)
+    pos = torch.tensor([32767, 20001], dtype=torch.int32, device="cuda")
+    plain = gemm.run_fused(x, w).float().cpu()
+    for impl, ww in (("B", w), ("A", gemm.permute_qkv_for_gemv(w))):
+        q = torch.zeros((M, Hq, 128), device="cuda").half()
+        kc = torch.zeros((M, Hkv, 32768, 128), device="cuda").half()
+        vc = torch.zeros_like(kc)
+        gemm.run_fused(x, ww, rope={"q_out": q, "k_cache": kc, "v_cache": vc, "pos": pos}, impl=impl)
+        torch.cuda.synchronize()
+        ref_q = tp._rope(plain[:, :Hq * 128].view(M, Hq, 128), pos.cpu(), 10000.0)
+        ref_k = tp._rope(plain[:, Hq * 128:(Hq + Hkv) * 128].view(M, Hkv, 128), pos.cpu(), 10000.0)
+        assert _rel(q.float().cpu(), ref_q) <= 2e-3, impl
+        got_k = kc[torch.arange(M), :, pos.long()].float().cpu()
+        assert _rel(got_k, ref_k) <= 2e-3, impl
