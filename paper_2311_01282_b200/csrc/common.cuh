@@ -93,10 +93,17 @@ fdpp_status make_kmajor_map(CUtensorMap *out, const void *ptr, int64_t rows, int
 __device__ __forceinline__ double rope_inv_freq(float theta, int i, int D) {
     return pow((double)theta, -2.0 * i / D);
 }
+// p * f with f = (hi, lo) float pair from the double; exact product error via
+// fma, Cody-Waite reduction by 2 pi in float (no per-element double math)
 __device__ __forceinline__ void rope_sincos(int p, double inv_freq, float *sn, float *cs) {
-    const double x = (double)p * inv_freq;
-    const double r = x - rint(x * 0.15915494309189535) * 6.283185307179586;
-    __sincosf((float)r, sn, cs);
+    const float f_hi = (float)inv_freq, f_lo = (float)(inv_freq - (double)f_hi);
+    const float pf = (float)p;                      // exact: p < 2^24
+    const float x_hi = pf * f_hi;
+    const float x_err = fmaf(pf, f_hi, -x_hi) + pf * f_lo;
+    const float k = rintf(x_hi * 0.159154943091895336f);
+    float r = fmaf(-k, 6.28318548202514648f, x_hi);  // 2 pi = hi + lo, hi = float(2 pi)
+    r = fmaf(-k, -1.74845553146951718e-07f, r) + x_err;
+    __sincosf(r, sn, cs);
 }
 
 // ------------------------------------------------------------- element types
