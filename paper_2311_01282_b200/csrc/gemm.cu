@@ -1193,7 +1193,11 @@ static fdpp_status plan_tc(const fdpp_gemm_params *p, bool swap, TcPlan *pl) {
     // CTAs per SM.  ctas < 0 forces cs = -ctas.
     pl->cluster = swap && ((p->ctas == 0 && tiles <= 2 * sms) || p->ctas < 0);
     if (pl->cluster) {
-        int cs = p->ctas < 0 ? -p->ctas : (tiles <= 40 ? 8 : tiles <= (sms * 9) / 10 ? 2 : 1);
+        // the largest power-of-two split that keeps every CTA in one wave at two
+        // per SM (the 7B shapes: 8 / 2 / 1 as measured; the 70B shards get 4-16)
+        int cs = 1;
+        while (cs < 16 && tiles * cs * 2 <= 2 * sms && kb_total / (cs * 2) >= 2) cs *= 2;
+        if (p->ctas < 0) cs = -p->ctas;
         cs = cs < 1 ? 1 : (cs > 16 ? 16 : cs);  // > 8: non-portable cluster size
         if (cs > kb_total) cs = kb_total;
         TcCluster &c = pl->ck;
