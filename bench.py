@@ -451,7 +451,10 @@ def run_gpu(args):
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(dom["gbs"] / peak, 4), "frac_of_8tbs": round(dom["gbs"] / 8000, 4),
                      "traffic": traffic, "bytes_per_launch": dom["bytes"],
-                     "us_per_launch": round(dom["s_per_launch"] * 1e6, 2)},
+                     "us_per_launch": round(dom["s_per_launch"] * 1e6, 2),
+                     # the cache grows one position per step; the attention bytes and
+                     # time are taken at this length, the ncu traffic at the start length
+                     "kv_len_at_measure": Lnow},
         "step_hbm": {"bytes": step_bytes, "achieved_gbs": round(step_bytes / (secs / K) / 1e9, 1),
                      "frac": round(step_bytes / (secs / K) / 1e9 / peak, 4)},
         "kernels": {n: {"us": round(o["s_per_launch"] * 1e6, 2), "gbs": round(o["gbs"], 1),
