@@ -908,12 +908,13 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV) {
     if constexpr (!ASYNC) {
         if (args.list_mode) {
+            // let the next kernel (the O projection) get resident and start its weight
+            // stream now, under the async launch's tail: its griddepcontrol.wait still
+            // waits for this whole grid, so the recomputed rows are visible to it
+            pdl_trigger();
             pdl_wait();  // the list comes from the async launch
             const int count = __ldcg(args.flag_count);
-            if (count == 0) {  // nothing flagged (the common case): no list to walk or clear
-                pdl_trigger();
-                return;
-            }
+            if (count == 0) return;  // nothing flagged (the common case): no list to walk or clear
             const int P = args.p * args.nsub;
             const int64_t items = (int64_t)count * args.n_rg * P;
             for (int64_t i = blockIdx.x; i < items; i += gridDim.x) {
@@ -925,7 +926,6 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
                 attn_cta<T, D, GT, ASYNC, MMA>(args, tmK, tmV, x, kvh * args.n_rg + rg, b);
                 __syncthreads();  // shared memory is reused by the next item
             }
-            pdl_trigger();
             // the last CTA clears the list and its dedupe markers (graph replay)
             __syncthreads();
             if (threadIdx.x == 0) {
