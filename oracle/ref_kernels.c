@@ -24,9 +24,11 @@
 #include <string.h>
 #include <unistd.h>
 
-/* Minimal dynamic-schedule parallel-for over [0, n) on pthreads (numba's
-   prange stand-in; the image's gcc has no usable OpenMP runtime).  Each task
-   index is executed exactly once; tasks own disjoint outputs. */
+/* Dynamic-schedule parallel-for over [0, n) on a persistent pthread pool
+   (numba's prange stand-in: numba's threading layer keeps its workers alive
+   between calls, so a per-call thread spawn would overstate the reference's
+   cost on small problems; the image's gcc has no usable OpenMP runtime).
+   Each task index is executed exactly once; tasks own disjoint outputs. */
 static int g_threads = 0;
 
 int oracle_set_threads(int n) {
@@ -39,16 +41,38 @@ int oracle_set_threads(int n) {
 }
 
 typedef void (*task_fn)(int64_t t, void *ctx);
-typedef struct { int64_t n; int64_t next; pthread_mutex_t mu; task_fn fn; void *ctx; } pool_t;
+
+static pthread_mutex_t g_mu = PTHREAD_MUTEX_INITIALIZER;
+static pthread_cond_t g_go = PTHREAD_COND_INITIALIZER, g_done = PTHREAD_COND_INITIALIZER;
+static pthread_mutex_t g_call = PTHREAD_MUTEX_INITIALIZER;  /* one parallel_for at a time */
+static int g_pool = 0;              /* workers started */
+static uint64_t g_gen = 0;          /* job generation */
+static int g_want = 0;              /* workers taking part in the current job */
+static int g_busy = 0;              /* of those, still running */
+static int64_t g_n = 0, g_next = 0;
+static task_fn g_fn = NULL;
+static void *g_ctx = NULL;
+
+static void run_tasks(void) {
+    for (;;) {
+        int64_t t = __atomic_fetch_add(&g_next, 1, __ATOMIC_RELAXED);
+        if (t >= g_n) break;
+        g_fn(t, g_ctx);
+    }
+}
 
 static void *worker(void *arg) {
-    pool_t *P = (pool_t *)arg;
+    const int id = (int)(intptr_t)arg;
+    uint64_t seen = 0;
+    pthread_mutex_lock(&g_mu);
     for (;;) {
-        pthread_mutex_lock(&P->mu);
-        int64_t t = P->next++;
-        pthread_mutex_unlock(&P->mu);
-        if (t >= P->n) break;
-        P->fn(t, P->ctx);
+        while (g_gen == seen) pthread_cond_wait(&g_go, &g_mu);
+        seen = g_gen;
+        if (id >= g_want) continue;     /* not part of this job */
+        pthread_mutex_unlock(&g_mu);
+        run_tasks();
+        pthread_mutex_lock(&g_mu);
+        if (--g_busy == 0) pthread_cond_signal(&g_done);
     }
     return NULL;
 }
@@ -57,13 +81,24 @@ static void parallel_for(int64_t n, task_fn fn, void *ctx) {
     int T = oracle_set_threads(0);
     if (T > n) T = (int)n;
     if (T <= 1) { for (int64_t t = 0; t < n; ++t) fn(t, ctx); return; }
-    pool_t P; P.n = n; P.next = 0; P.fn = fn; P.ctx = ctx;
-    pthread_mutex_init(&P.mu, NULL);
-    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)T);
-    for (int i = 0; i < T; ++i) pthread_create(&th[i], NULL, worker, &P);
-    for (int i = 0; i < T; ++i) pthread_join(th[i], NULL);
-    free(th);
-    pthread_mutex_destroy(&P.mu);
+    pthread_mutex_lock(&g_call);
+    pthread_mutex_lock(&g_mu);
+    while (g_pool < T - 1) {            /* grow the pool (workers never exit) */
+        pthread_t th;
+        pthread_create(&th, NULL, worker, (void *)(intptr_t)g_pool);
+        pthread_detach(th);
+        ++g_pool;
+    }
+    g_n = n; g_next = 0; g_fn = fn; g_ctx = ctx;
+    g_want = T - 1; g_busy = T - 1;
+    ++g_gen;
+    pthread_cond_broadcast(&g_go);
+    pthread_mutex_unlock(&g_mu);
+    run_tasks();                        /* the calling thread is worker T-1 */
+    pthread_mutex_lock(&g_mu);
+    while (g_busy > 0) pthread_cond_wait(&g_done, &g_mu);
+    pthread_mutex_unlock(&g_mu);
+    pthread_mutex_unlock(&g_call);
 }
 
 /* attention.py:167-199 (_async_partials_njit): per (row r, chunk j) task. */

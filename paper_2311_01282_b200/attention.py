@@ -43,22 +43,40 @@ class PartialAttnState(NamedTuple):
         return self.overflow_index >= 0
 
 
+AUTO = "auto"  # AttentionConfig.p: let the library plan the split for 148 SMs
+
+
 @dataclass(frozen=True)
 class AttentionConfig:
-    """p = semantic split count (chunk_bounds(L, p)); None/0 = choose for 148
-    SMs.  splits_per_chunk = CTAs per chunk (0 = auto); it never changes
-    results beyond fp32 summation order, and never changes flags."""
+    """p = semantic split count (chunk_bounds(L, p)), validated like the
+    reference (attention.py:46-56: an int >= 1, else ValueError); the B200
+    extension ``p=AUTO`` ("auto", or ``AttentionConfig.auto(...)``) lets the
+    library choose p for the machine.  splits_per_chunk = CTAs per chunk
+    (0 = auto); it never changes results beyond fp32 summation order, and
+    never changes flags."""
 
-    p: Optional[int]
+    p: object
     scale: float
     calib: Optional[ScalingCalibration] = None
     splits_per_chunk: int = 0
 
     def __post_init__(self):
-        if self.p is not None and self.p != 0 and self.p < 1:
-            raise ValueError(f"partition count must be >= 1, got {self.p}")
+        if self.p != AUTO:
+            if isinstance(self.p, bool) or not isinstance(self.p, (int, np.integer)):
+                raise ValueError(f"partition count must be an int >= 1 or {AUTO!r}, got {self.p!r}")
+            if self.p < 1:
+                raise ValueError(f"partition count must be >= 1, got {self.p}")
         if not self.scale > 0:
             raise ValueError(f"scale must be > 0, got {self.scale}")
+
+    @classmethod
+    def auto(cls, scale: float, calib: Optional[ScalingCalibration] = None, splits_per_chunk: int = 0):
+        return cls(p=AUTO, scale=scale, calib=calib, splits_per_chunk=splits_per_chunk)
+
+    @property
+    def p_code(self) -> int:
+        """The C ABI's p (0 = auto)."""
+        return 0 if self.p == AUTO else int(self.p)
 
 
 class AttnStats:
@@ -153,7 +171,7 @@ def _params(q, k, v, o, cfg, mode, L):
     prm.scale = float(cfg.scale)
     if cfg.calib is not None:
         prm.phi, prm.a, prm.b = float(cfg.calib.phi), float(cfg.calib.a), float(cfg.calib.b)
-    prm.p = int(cfg.p or 0)
+    prm.p = cfg.p_code
     prm.splits_per_chunk = int(cfg.splits_per_chunk or 0)
     prm.mode = _lib.ATTN_ASYNC if mode == "async" else _lib.ATTN_SYNC
     return prm
@@ -207,7 +225,7 @@ def decode_attention(q, k_cache, v_cache, cfg: AttentionConfig, mode: str = "asy
     lib = _lib.load()
     need = ctypes.c_size_t()
     _lib.check(lib.fdpp_attn_workspace_size(ctypes.byref(prm), ctypes.byref(need)), "attention")
-    ws = workspace.get(need.value, q.device, tag="attn")
+    ws = workspace.get(need.value, q.device, tag="attn", stream=stream)
     prm.workspace, prm.workspace_bytes = ws.data_ptr(), ws.numel()
     c, s = ctypes.c_int32(), ctypes.c_int32()
     _lib.check(lib.fdpp_attn_plan(ctypes.byref(prm), ctypes.byref(c), ctypes.byref(s)), "attention")
@@ -346,7 +364,7 @@ def async_partials(Q, K, V, cfg: AttentionConfig):
     whose state is not f32-representable reports its lower bound."""
     if cfg.calib is None:
         raise ValueError("async mode requires a ScalingCalibration")
-    if not cfg.p:
+    if cfg.p == AUTO:
         raise ValueError("async_partials needs an explicit p")
     _, _, ex, _ = _single_head(Q, K, V, cfg, "async", want_partials=True)
     return (ex["num"].cpu().numpy(), ex["den"].cpu().numpy(),
@@ -375,7 +393,7 @@ def sample_logits(q, k_cache, scale: float, n: int, *, seq_lens=None, seed: int 
     _lib.require_cuda()
     if n < 1:
         raise ValueError("n must be >= 1")
-    prm = _params(q, k_cache, k_cache, q, AttentionConfig(p=0, scale=scale), "sync", None)
+    prm = _params(q, k_cache, k_cache, q, AttentionConfig.auto(scale), "sync", None)
     if seq_lens is not None:
         if seq_lens.dtype != torch.int32 or not seq_lens.is_cuda:
             raise ValueError("seq_lens must be an int32 CUDA tensor")

@@ -19,6 +19,8 @@ namespace fdpp {
 void set_error(const char *fmt, ...);
 fdpp_status cuda_status(cudaError_t e, const char *what);
 int sm_count();
+// f32 CUDA-core flat-GEMM family (gemm_f32.cu): reference-precision calls
+fdpp_status run_gemm_f32(int impl, const fdpp_gemm_params *p, cudaStream_t st);
 
 #define FDPP_CHECK_LAUNCH(what)                                     \
     do {                                                            \
@@ -378,6 +380,10 @@ __device__ __forceinline__ int4 ld_stream_16(const void *p) {
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p), "l"(kEvictFirst));
     return r;
+}
+__device__ __forceinline__ float4 ld_stream_16f(const void *p) {
+    const int4 r = ld_stream_16(p);
+    return make_float4(__int_as_float(r.x), __int_as_float(r.y), __int_as_float(r.z), __int_as_float(r.w));
 }
 
 }  // namespace fdpp

@@ -45,6 +45,9 @@ __global__ void rope_append_kernel(const T *__restrict__ qkv, T *__restrict__ q_
     const int width = (Hq + 2 * Hkv) * D;
     const T *row = qkv + (int64_t)b * width;
     const int p = pos[b];
+    // capacity guard: a [B, Hkv, Lmax, D] cache holds csh / D rows per head; a
+    // position past it is never written (it would land in the next head / row)
+    const bool in_cache = p >= 0 && (int64_t)p < csh / D;
     for (int idx = threadIdx.x; idx < (Hq + Hkv) * half; idx += blockDim.x) {
         const int h = idx / half, i = idx % half;
         const double inv_freq = rope_inv_freq(theta, i, D);
@@ -57,14 +60,14 @@ __global__ void rope_append_kernel(const T *__restrict__ qkv, T *__restrict__ q_
             T *dst = q_out + ((int64_t)b * Hq + h) * D;
             dst[i] = r0;
             dst[i + half] = r1;
-        } else {
+        } else if (in_cache) {
             T *dst = kc + (int64_t)b * csb + (int64_t)(h - Hq) * csh + (int64_t)p * D;
             dst[i] = r0;
             dst[i + half] = r1;
         }
     }
     const T *vsrc = row + (Hq + Hkv) * D;
-    for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x) {
+    for (int idx = threadIdx.x; in_cache && idx < Hkv * D; idx += blockDim.x) {
         const int h = idx / D, i = idx % D;
         vc[(int64_t)b * csb + (int64_t)h * csh + (int64_t)p * D + i] = vsrc[h * D + i];
     }

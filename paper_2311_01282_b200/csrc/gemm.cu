@@ -349,8 +349,11 @@ gemv_fused_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ W,
                                (int64_t)(hd - fz.Hq) * fz.cache_sh + (int64_t)p * 128
                          : static_cast<T *>(fz.v_cache) + (int64_t)m * fz.cache_sb +
                                (int64_t)(hd - fz.Hq - fz.Hkv) * fz.cache_sh + (int64_t)p * 128;
-            dst[i] = Elem<T>::from_f(lo);
-            dst[i + 64] = Elem<T>::from_f(hi);
+            // capacity guard: cache rows per head = cache_sh / 128 (never write past it)
+            if (hd < fz.Hq || (p >= 0 && (int64_t)p < fz.cache_sh / 128)) {
+                dst[i] = Elem<T>::from_f(lo);
+                dst[i + 64] = Elem<T>::from_f(hi);
+            }
         }
     }
 }
@@ -1064,7 +1067,8 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
                     dst = static_cast<T *>(fz.v_cache) + (int64_t)m * fz.cache_sb +
                           (int64_t)(tn - fz.Hq - fz.Hkv) * fz.cache_sh + (int64_t)p * 128;
                 }
-                dst[row] = Elem<T>::from_f(val);
+                // capacity guard: cache rows per head = cache_sh / 128
+                if (tn < fz.Hq || (p >= 0 && (int64_t)p < fz.cache_sh / 128)) dst[row] = Elem<T>::from_f(val);
             }
         }
     }
@@ -1474,6 +1478,10 @@ extern "C" fdpp_status fdpp_prepack_weight(const void *b_kn, void *w_nk, int32_t
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     dim3 grid(ceil_div(N, 32), ceil_div(ldw, 32)), block(32, 8);
     switch (dtype) {
+        case FDPP_F32:
+            prepack_kernel<float><<<grid, block, 0, st>>>(static_cast<const float *>(b_kn),
+                                                          static_cast<float *>(w_nk), K, N, ldw);
+            break;
         case FDPP_F16:
             prepack_kernel<__half><<<grid, block, 0, st>>>(static_cast<const __half *>(b_kn),
                                                            static_cast<__half *>(w_nk), K, N, ldw);
@@ -1493,7 +1501,7 @@ extern "C" fdpp_status fdpp_gemm_workspace_size(int32_t impl, const fdpp_gemm_pa
                                                 size_t *bytes) {
     FDPP_REQUIRE(p && bytes, FDPP_ERR_VALUE, "null pointer");
     *bytes = 0;
-    if (impl == FDPP_IMPL_A) return FDPP_OK;
+    if (impl == FDPP_IMPL_A || p->dtype == FDPP_F32) return FDPP_OK;
     FDPP_REQUIRE(impl == FDPP_IMPL_B || impl == FDPP_IMPL_C, FDPP_ERR_VALUE, "bad impl %d", impl);
     TcPlan pl;
     fdpp_status s = plan_tc(p, impl == FDPP_IMPL_B, &pl);
@@ -1503,6 +1511,7 @@ extern "C" fdpp_status fdpp_gemm_workspace_size(int32_t impl, const fdpp_gemm_pa
 }
 
 extern "C" fdpp_status fdpp_impl_a_gemv(const fdpp_gemm_params *p, void *stream) {
+    if (p && p->dtype == FDPP_F32) return run_gemm_f32(FDPP_IMPL_A, p, static_cast<cudaStream_t>(stream));
     fdpp_status s = check_gemm(p);
     if (s != FDPP_OK) return s;
     FDPP_REQUIRE(p->M <= 8, FDPP_ERR_SHAPE, "ImplA (GEMV) supports M <= 8, got %d", p->M);
@@ -1514,10 +1523,12 @@ extern "C" fdpp_status fdpp_impl_a_gemv(const fdpp_gemm_params *p, void *stream)
 }
 
 extern "C" fdpp_status fdpp_impl_b_flat(const fdpp_gemm_params *p, void *stream) {
+    if (p && p->dtype == FDPP_F32) return run_gemm_f32(FDPP_IMPL_B, p, static_cast<cudaStream_t>(stream));
     return run_tc(p, true, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" fdpp_status fdpp_impl_c_gemm(const fdpp_gemm_params *p, void *stream) {
+    if (p && p->dtype == FDPP_F32) return run_gemm_f32(FDPP_IMPL_C, p, static_cast<cudaStream_t>(stream));
     return run_tc(p, false, static_cast<cudaStream_t>(stream));
 }
 

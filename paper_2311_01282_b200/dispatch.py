@@ -72,7 +72,7 @@ def impl_a_gemv(a, b, **kw):
     if a.shape[1] != (b.K if isinstance(b, _g.PackedWeight) else b.shape[0]):
         raise ShapeError(f"inner dims disagree: {tuple(a.shape)} x {tuple(getattr(b, 'shape', ()))}")
     M = a.shape[0]
-    if M <= GEMV_MAX_M:
+    if M <= GEMV_MAX_M or _g.reference_dtype(a) == _torch_f32():
         return _g.reference_call(_g.IMPL_A, a, b, **kw)
     pw = _g.as_packed(b, _dtype_of(a))
     parts = [_g.reference_call(_g.IMPL_A, a[i:i + GEMV_MAX_M], pw) for i in range(0, M, GEMV_MAX_M)]
@@ -83,10 +83,12 @@ def impl_a_gemv(a, b, **kw):
 
 
 def _dtype_of(a):
+    return _g.reference_dtype(a)
+
+
+def _torch_f32():
     import torch
-    if isinstance(a, torch.Tensor) and a.dtype in (torch.float16, torch.bfloat16):
-        return a.dtype
-    return torch.float16
+    return torch.float32
 
 
 def impl_b_flat(a, b, workers: int = None, **kw):

@@ -1,10 +1,11 @@
 """Device GEMM plumbing shared by flatgemm.py and dispatch.py.
 
 C[M,N] = A[M,K] · B[K,N] with B prepacked once into W[N, ldw] (K-major, the
-layout both the GEMV and the tcgen05 TMA tiles stream), fp16/bf16 storage,
-fp32 accumulation.  Reference-API calls with numpy f32 operands are rounded
-to fp16 on the device (the precision the B200 path computes in; north_star:
-"fp16/bf16 with fp32 accumulation", 2e-3 relative bar).
+layout both the GEMV and the tcgen05 TMA tiles stream).  fp16/bf16 operands
+run on the tensor-core / GEMV hot path (fp32 accumulation, the north_star's
+2e-3 bar); float32 operands -- the reference API's numpy f32 arrays or f32
+CUDA tensors -- run the f32 CUDA-core forms of the same three impls
+(csrc/gemm_f32.cu), keeping the reference's own <= 1e-4 contract.
 """
 
 from __future__ import annotations
@@ -57,7 +58,7 @@ def pack_weight(b_kn, dtype=None, stream=None) -> PackedWeight:
     if not isinstance(b_kn, torch.Tensor):
         b_kn = torch.from_numpy(np.ascontiguousarray(b_kn, dtype=np.float32)).cuda()
     if dtype is None:
-        dtype = b_kn.dtype if b_kn.dtype in (torch.float16, torch.bfloat16) else torch.float16
+        dtype = b_kn.dtype if b_kn.dtype in (torch.float16, torch.bfloat16, torch.float32) else torch.float32
     b = b_kn.to(device="cuda", dtype=dtype).contiguous()
     if b.dim() != 2:
         raise ShapeError("weight must be 2-D [K, N]")
@@ -138,11 +139,20 @@ def run(impl: int, a, pw: PackedWeight, *, out=None, residual=None, block_x=0, c
     need = ctypes.c_size_t()
     _lib.check(lib.fdpp_gemm_workspace_size(impl, ctypes.byref(prm), ctypes.byref(need)), "gemm")
     if need.value:
-        ws = workspace.get(need.value, a.device, tag=ws_tag)
+        ws = workspace.get(need.value, a.device, tag=ws_tag, stream=stream)
         prm.workspace, prm.workspace_bytes = ws.data_ptr(), ws.numel()
     _lib.check(lib.fdpp_run_kernel(impl, ctypes.byref(prm), _lib.stream_handle(stream)),
                ("ImplA", "ImplB", "ImplC")[impl])
     return out
+
+
+def reference_dtype(a):
+    """Device dtype of a reference-signature call: fp16/bf16 tensors keep their
+    dtype (tensor-core path); numpy arrays and float32 tensors compute in f32."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor) and a.dtype in (torch.float16, torch.bfloat16):
+        return a.dtype
+    return torch.float32
 
 
 def reference_call(impl: int, a, b, **kw):
@@ -152,9 +162,7 @@ def reference_call(impl: int, a, b, **kw):
     if a.shape[1] != (b.K if isinstance(b, PackedWeight) else b.shape[0]):
         raise ShapeError(f"inner dims disagree: {tuple(a.shape)} x {tuple(getattr(b, 'shape', (b.K, b.N)))}")
     was_numpy = not isinstance(a, torch.Tensor)
-    dtype = torch.float16
-    if isinstance(a, torch.Tensor) and a.dtype in (torch.float16, torch.bfloat16):
-        dtype = a.dtype
+    dtype = reference_dtype(a)
     pw = as_packed(b, dtype)
     A = as_activation(a, dtype)
     if A.shape[1] != pw.ldw:
@@ -260,7 +268,7 @@ def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ss
     need = ctypes.c_size_t()
     _lib.check(lib.fdpp_gemm_workspace_size(IMPL_B, ctypes.byref(prm), ctypes.byref(need)), "gemm_fused")
     if need.value:
-        ws = workspace.get(need.value, a.device, tag=ws_tag)
+        ws = workspace.get(need.value, a.device, tag=ws_tag, stream=stream)
         prm.workspace, prm.workspace_bytes = ws.data_ptr(), ws.numel()
     _lib.check(lib.fdpp_gemm_fused(ctypes.byref(prm), ctypes.byref(fz), _lib.stream_handle(stream)),
                "gemm_fused")

@@ -185,7 +185,7 @@ class LlamaDecoder:
         self.ssq_b = torch.zeros_like(self.ssq_a)
         self.ssq_tiles = nt
         self.recomputed = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.attn_cfg = AttentionConfig(p=attn_p, scale=1.0 / math.sqrt(Dh), calib=calib,
+        self.attn_cfg = AttentionConfig(p=attn_p or "auto", scale=1.0 / math.sqrt(Dh), calib=calib,
                                         splits_per_chunk=attn_splits)
         if table is None:
             table = build_dispatch_table(cfg, dtype=dtype, tp=tp_size)
@@ -211,6 +211,7 @@ class LlamaDecoder:
         if tp_size > 1 and not fused:
             raise NotImplementedError("tensor parallelism runs on the fused (ImplB) decode step")
         self.graph = None
+        self._host_pos = None    # host mirror of the decode position (prefill_random / rewind)
         self._layer_hook = None  # calibrate(): samples attention inputs after each QKV
         if fused:  # fold the RMSNorm weights into the following projections' columns
             for L in self.layers:
@@ -272,6 +273,22 @@ class LlamaDecoder:
         self.pos.fill_(L)
         self.lens.fill_(L + 1)
         self.ids.random_(0, self.cfg.vocab, generator=g)
+        self._host_pos = L
+
+    def rewind(self, L: int):
+        """Move every sequence back to position L (the next token is written at
+        row L again); the KV rows [0, L) are kept."""
+        if not 0 <= L < self.max_len:
+            raise ValueError(f"position {L} outside the cache (max_len {self.max_len})")
+        self.pos.fill_(L)
+        self.lens.fill_(L + 1)
+        self._host_pos = L
+
+    @property
+    def steps_left(self):
+        """Decode steps the KV cache still has rows for (None: positions were set
+        directly on the device and are not tracked on the host)."""
+        return None if self._host_pos is None else self.max_len - self._host_pos
 
     # ------------------------------------------------------------------ one step
     def _gemm(self, op, a, pw, out, residual=None):
@@ -393,9 +410,16 @@ class LlamaDecoder:
         return g
 
     def step(self):
+        # every step appends one KV row at `pos`: refuse to run past the cache
+        # (the append kernels also skip rows >= max_len, so nothing is corrupted)
+        if self._host_pos is not None and self._host_pos >= self.max_len:
+            raise RuntimeError(f"KV cache full: position {self._host_pos} >= max_len {self.max_len}; "
+                               "rewind() or allocate a longer cache")
         if self.graph is None:
             self.capture()
         self.graph.replay()
+        if self._host_pos is not None:
+            self._host_pos += 1
 
     def decode(self, ids_host, out_host):
         """End-to-end step through the public API: H2D copy of this step's token

@@ -75,7 +75,7 @@ def _worker(rank, world, port, q):
         dec.lens.copy_(pos + 1)
         dec.enqueue_step()      # eager: the gloo all-reduce is not graph-capturable
         torch.cuda.synchronize()
-        q.put((rank, dec.x.float().cpu(), dec.ids.cpu()))
+        q.put((rank, dec.x.float().cpu().numpy(), dec.ids.cpu().numpy()))  # by value
     finally:
         dist.destroy_process_group()
 
@@ -121,7 +121,7 @@ def test_tp2_step_matches_unsharded():
         p.join(timeout=120)
         assert p.exitcode == 0
     for rank, x, nxt in got:
-        err = float((np.abs(x.numpy() - x_ref.numpy()).max(1) / np.abs(x_ref.numpy()).max(1)).max())
+        err = float((np.abs(x - x_ref.numpy()).max(1) / np.abs(x_ref.numpy()).max(1)).max())
         assert err <= 2e-2, f"rank {rank}: rel err {err}"
     # the replicated LM head + argmax agree across ranks
-    assert torch.equal(got[0][2], got[1][2])
+    assert np.array_equal(got[0][2], got[1][2])

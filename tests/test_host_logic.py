@@ -157,6 +157,11 @@ def test_config_and_band_validation():
         fd.ScalingCalibration(phi=0.0, a=-1.0, b=95.0, coverage=1.0)
     with pytest.raises(ValueError):
         fd.AttentionConfig(p=-1, scale=1.0)
+    for bad in (0, None, 1.5, "4"):  # the reference's p >= 1 validation (attention.py:46-56)
+        with pytest.raises(ValueError):
+            fd.AttentionConfig(p=bad, scale=1.0)
+    assert fd.AttentionConfig.auto(1.0).p == fd.AUTO and fd.AttentionConfig.auto(1.0).p_code == 0
+    assert fd.AttentionConfig(p=3, scale=1.0).p_code == 3
     with pytest.raises(ValueError):
         fd.AttentionConfig(p=2, scale=0.0)
     c = fd.ScalingCalibration(phi=6.0, a=-3.0, b=3.0, coverage=1.0)

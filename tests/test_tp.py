@@ -71,7 +71,10 @@ def _worker(rank, world, port, q):
                                    rank=rank, all_reduce=dist.all_reduce)
             kc[li][:, rank * s.n_kv_heads:(rank + 1) * s.n_kv_heads] = kcs
             vc[li][:, rank * s.n_kv_heads:(rank + 1) * s.n_kv_heads] = vcs
-        q.put((rank, x, [k[:, rank * s.n_kv_heads:(rank + 1) * s.n_kv_heads] for k in kc]))
+        # numpy copies travel by value: a shared-memory tensor would need the
+        # worker alive until the parent has unpickled it
+        q.put((rank, x.numpy().copy(),
+               [k[:, rank * s.n_kv_heads:(rank + 1) * s.n_kv_heads].numpy().copy() for k in kc]))
     finally:
         dist.destroy_process_group()
 
@@ -91,6 +94,7 @@ def test_tp_layer_matches_unsharded(world):
         assert p.exitcode == 0
     s = tp.shard_dims(TINY, world)
     for rank, x, kcs in got:
+        x, kcs = torch.from_numpy(x), [torch.from_numpy(k) for k in kcs]
         assert torch.allclose(x, ref_x, atol=2e-4, rtol=2e-4), f"rank {rank}: residual stream differs"
         for li in range(TINY.n_layers):  # each rank appended its own KV heads' rows
             exp = ref_kc[li][:, rank * s.n_kv_heads:(rank + 1) * s.n_kv_heads]

@@ -23,7 +23,7 @@ for B, L in shapes:
     out = torch.empty_like(q)
     byt = B * H * L * D * 4 + 2 * B * H * D * 2
     for p, spc in ((0, 0), (1, 1), (2, 1), (3, 1), (4, 1), (6, 1), (8, 1), (1, 2), (1, 4)):
-        cfg = fd.AttentionConfig(p=p, scale=1 / math.sqrt(D), calib=cal, splits_per_chunk=spc)
+        cfg = fd.AttentionConfig(p=p or "auto", scale=1 / math.sqrt(D), calib=cal, splits_per_chunk=spc)
         it = [0]
 
         def f():

@@ -21,7 +21,7 @@ lib.fdpp_atrace_read.argtypes = [ctypes.c_void_p]
 B, Hq, Hkv, L = (int(x) for x in sys.argv[1:5])
 D = 128
 cal = fd.ScalingCalibration(phi=-7.775933742523193, a=-1.0, b=16.577659606933594, coverage=1.0)
-cfg = fd.AttentionConfig(p=0, scale=1 / math.sqrt(D), calib=cal)
+cfg = fd.AttentionConfig.auto(1 / math.sqrt(D), cal)
 q = torch.randn((B, Hq, D), device="cuda").half()
 k = torch.randn((B, Hkv, L, D), device="cuda").half()
 v = torch.randn((B, Hkv, L, D), device="cuda").half()

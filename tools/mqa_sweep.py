@@ -17,7 +17,7 @@ for B, Hq, Hkv, L in ((8, 32, 2, 32768), (32, 8, 1, 1024), (32, 16, 2, 1024), (3
     out = torch.empty_like(q)
     byt = B * Hkv * L * D * 4 + 2 * B * Hq * D * 2
     for p, spc in ((0, 0), (2, 1), (4, 1), (8, 1), (16, 1), (20, 1), (24, 1), (27, 1), (32, 1)):
-        cfg = fd.AttentionConfig(p=p, scale=1 / math.sqrt(D), calib=cal, splits_per_chunk=spc)
+        cfg = fd.AttentionConfig(p=p or "auto", scale=1 / math.sqrt(D), calib=cal, splits_per_chunk=spc)
         plan = fd.attention.plan(q, k, cfg)
         med, _ = median_mad(measure(lambda: fd.decode_attention(q, k, v, cfg, "async", out=out), reps=10, warmup=2))
         print(f"B={B} Hq={Hq} Hkv={Hkv} L={L} p={p} plan={plan} {med*1e6:8.1f} us {byt/med/1e9:7.0f} GB/s", flush=True)

@@ -11,7 +11,7 @@ B, H, L, D = (int(x) for x in (sys.argv[1:5] if len(sys.argv) > 4 else (32, 32, 
 Hkv = int(sys.argv[5]) if len(sys.argv) > 5 else H
 reps = int(sys.argv[6]) if len(sys.argv) > 6 else 3
 cal = fd.ScalingCalibration(phi=-7.775933742523193, a=-1.0, b=16.577659606933594, coverage=1.0)
-cfg = fd.AttentionConfig(p=0, scale=1 / math.sqrt(D), calib=cal)
+cfg = fd.AttentionConfig.auto(1 / math.sqrt(D), cal)
 caches = []
 for i in range(3):
     k = torch.randn((B, Hkv, L, D), device="cuda").half()
