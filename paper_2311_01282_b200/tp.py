@@ -120,20 +120,23 @@ def _rope(x, pos, theta):
     import torch
     D = x.shape[-1]
     half = D // 2
-    inv = theta ** (-2.0 * torch.arange(half, dtype=torch.float64) / D)
-    ang = pos.double()[:, None] * inv[None, :]
+    inv = theta ** (-2.0 * torch.arange(half, dtype=torch.float64, device=x.device) / D)
+    ang = pos.to(x.device).double()[:, None] * inv[None, :]
     cos, sin = ang.cos().float()[:, None, :], ang.sin().float()[:, None, :]
     x0, x1 = x[..., :half], x[..., half:]
     return torch.cat([x0 * cos - x1 * sin, x1 * cos + x0 * sin], -1)
 
 
-def reference_layer(x, L: dict, kc, vc, pos, lens, cfg, n_heads, n_kv_heads, *, rank=0, all_reduce=None):
-    """One decode layer in fp32 on (possibly sharded) weights.
+def reference_layer(x, L: dict, kc, vc, pos, lens, cfg, n_heads, n_kv_heads, *, rank=0, all_reduce=None,
+                    trace=None):
+    """One decode layer in fp32 on (possibly sharded) weights, on x's device.
 
     x [B, hidden]; L: qkv [Nq, hidden], o [hidden, Hq_l D], gate_up, down, ln1,
     ln2; kc/vc [B, Hkv_l, Lmax, D] (row pos[b] is written); lens [B] attended
     lengths (pos + 1).  With all_reduce (tp > 1) the O / down outputs are
-    partials: rank 0 adds the residual, then all_reduce sums them in place."""
+    partials: rank 0 adds the residual, then all_reduce sums them in place.
+    trace: optional dict receiving the intermediates q, k, v (after RoPE) and
+    att (the attention output)."""
     import torch
     B = x.shape[0]
     D = cfg.head_dim
@@ -147,13 +150,16 @@ def reference_layer(x, L: dict, kc, vc, pos, lens, cfg, n_heads, n_kv_heads, *, 
         kc[b, :, int(pos[b])] = k[b]
         vc[b, :, int(pos[b])] = v[b]
     G = n_heads // n_kv_heads
-    att = torch.empty((B, n_heads, D))
+    att = torch.empty((B, n_heads, D), device=x.device)
     for b in range(B):
         n = int(lens[b])
-        for hq in range(n_heads):
-            s = (kc[b, hq // G, :n].float() @ q[b, hq]) / math.sqrt(D)
-            p = torch.softmax(s.double(), 0).float()
-            att[b, hq] = p @ vc[b, hq // G, :n].float()
+        kb = kc[b, :, :n].float().repeat_interleave(G, 0)            # [Hq, n, D]
+        vb = vc[b, :, :n].float().repeat_interleave(G, 0)
+        s = torch.einsum("hnd,hd->hn", kb, q[b]) / math.sqrt(D)
+        p = torch.softmax(s.double(), -1).float()
+        att[b] = torch.einsum("hn,hnd->hd", p, vb)
+    if trace is not None:
+        trace.update(q=q, k=k, v=v, att=att)
     o = att.view(B, n_heads * D) @ L["o"].float().T
     x = x + o if all_reduce is None else (x + o if rank == 0 else o)
     if all_reduce is not None:

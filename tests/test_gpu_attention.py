@@ -272,7 +272,7 @@ def test_ragged_seq_lens(fd, torch, Hkv, p):
     q, k, v = _qkv(torch, B, Hq, Hkv, L, D, 21 + Hkv, torch.float16)
     lens = torch.tensor([300, 1, 77, 129], dtype=torch.int32, device="cuda")
     calib = fd.ScalingCalibration(*GOLD_CAL, coverage=1.0)
-    cfg = fd.AttentionConfig(p=p, scale=1 / math.sqrt(D), calib=calib)
+    cfg = fd.AttentionConfig(p=p or fd.AUTO, scale=1 / math.sqrt(D), calib=calib)
     o, st = fd.decode_attention(q, k, v, cfg, "async", seq_lens=lens)
     G = Hq // Hkv
     qn, kn, vn = (t.float().cpu().numpy() for t in (q, k, v))

@@ -1,0 +1,150 @@
+"""Drive every libfdpp kernel once, small, for compute-sanitizer.
+
+    compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} \
+        --error-exitcode 1 python tools/sanitize.py
+
+Covers: attention (MHA CUDA-core async with cluster join and with the global
+ticket join + per-chunk outputs, sync mode, the list-mode recompute with
+flagged rows; GQA/MQA tensor-core async with cluster join, injected rows and
+the tensor-core recompute, tensor-core sync mode), ImplA GEMV, ImplB (cluster
+split-K, stream-K), ImplC, the f32 forms, the fused GEMM prologues/epilogues,
+the fused GEMV, the decode-step glue and vector softmax kernels, and a tiny
+decode step captured into a CUDA graph and replayed (workspace counters and
+the recompute list must be left clean across replays).
+"""
+
+import importlib
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2311_01282_b200 as fd  # noqa: E402
+from paper_2311_01282_b200 import _lib, gemm, llama  # noqa: E402
+
+D = importlib.import_module("paper_2311_01282_b200.dispatch")
+torch.cuda.set_device(0)
+g = torch.Generator(device="cuda").manual_seed(0)
+cal = fd.ScalingCalibration(phi=-7.775933742523193, a=-1.0, b=16.577659606933594, coverage=1.0)
+
+
+def step(name):
+    torch.cuda.synchronize()
+    print(f"ok  {name}", flush=True)
+
+
+def attn_case(B, Hq, Hkv, L, p, inject, **kw):
+    q = torch.randn((B, Hq, 128), generator=g, device="cuda").half()
+    k = torch.randn((B, Hkv, L, 128), generator=g, device="cuda").half()
+    v = torch.randn((B, Hkv, L, 128), generator=g, device="cuda").half()
+    for b, h in inject:
+        k[b, h, L // 3].mul_(40.0)
+    cfg = fd.AttentionConfig(p=p, scale=1 / math.sqrt(128), calib=cal)
+    for mode in ("async", "sync"):
+        fd.decode_attention(q, k, v, cfg, mode, **kw)
+    return q, k, v, cfg
+
+
+# ---- subsystem 1
+attn_case(2, 8, 8, 700, fd.AUTO, [(0, 1), (1, 5)])                     # MHA, cluster join, recompute
+q, k, v, cfg = attn_case(1, 4, 4, 600, 3, [(0, 2)])
+viol = torch.empty((1, 4, 3), dtype=torch.int32, device="cuda")
+num = torch.empty((1, 4, 3, 128), device="cuda")
+den = torch.empty((1, 4, 3), device="cuda")
+fd.decode_attention(q, k, v, cfg, "async", viol_index=viol, chunk_num=num, chunk_den=den)  # global join
+cfg2 = fd.AttentionConfig(p=2, scale=cfg.scale, calib=cal, splits_per_chunk=3)
+fd.decode_attention(q, k, v, cfg2, "async")                               # sub-range splits
+step("attention MHA (cluster join, global join, splits, recompute list, sync)")
+attn_case(2, 32, 2, 1500, fd.AUTO, [(1, 0)])                             # MQA tensor cores + recompute
+attn_case(1, 16, 2, 900, 5, [])                                          # G = 8, explicit p
+lens = torch.tensor([900, 3], dtype=torch.int32, device="cuda")
+q, k, v, cfg = attn_case(2, 16, 2, 900, fd.AUTO, [(0, 0)], seq_lens=lens)  # ragged lengths
+step("attention GQA/MQA tensor cores (async, sync, injected, ragged)")
+
+# ---- subsystem 2
+for M in (1, 3, 8, 17, 64):
+    a = torch.randn((M, 1024), generator=g, device="cuda").half()
+    b = (torch.randn((1024, 1536), generator=g, device="cuda") / 32).half()
+    pw = fd.pack_weight(b)
+    for ch in (D.KernelChoice.IMPL_A, D.KernelChoice.IMPL_B, D.KernelChoice.IMPL_C):
+        if ch == D.KernelChoice.IMPL_A and M > 8:
+            continue
+        D.run_device(ch, a, pw)
+    for ctas in (5, 150, -2, -8):
+        D.run_device(D.KernelChoice.IMPL_B, a, pw, ctas=ctas)
+    D.run_device(D.KernelChoice.IMPL_B, a, pw, stages=1)
+    fd.impl_b_flat(a.float().cpu().numpy(), b.float().cpu().numpy())   # f32 path
+    fd.impl_c_blocked(a.float(), b.float())
+step("ImplA / ImplB (cluster, stream-K) / ImplC / f32")
+
+B, H, Hq, Hkv = 4, 1024, 4, 2
+x = torch.randn((B, H), generator=g, device="cuda").half()
+ssq = torch.zeros((H // 128, B), device="cuda")
+po = gemm.PackedWeight((torch.randn((H, H), generator=g, device="cuda") / 32).half(), H, H)
+gemm.run_fused(x, po, out=x, residual=x, ssq_out=ssq)
+w_ln = torch.ones(H, dtype=torch.half, device="cuda")
+pq = gemm.PackedWeight((torch.randn(((Hq + 2 * Hkv) * 128, H), generator=g, device="cuda") / 32).half(),
+                       H, (Hq + 2 * Hkv) * 128)
+gemm.run_fused(x, pq, x_op=1, ssq_in=ssq, ssq_tiles=H // 128, norm_w=w_ln, eps=1e-5)
+kc = torch.zeros((B, Hkv, 64, 128), dtype=torch.half, device="cuda")
+vc = torch.zeros_like(kc)
+qo = torch.zeros((B, Hq, 128), dtype=torch.half, device="cuda")
+pos = torch.tensor([3, 17, 0, 63], dtype=torch.int32, device="cuda")
+gemm.run_fused(x, pq, x_op=3, ssq_in=ssq, ssq_tiles=H // 128, eps=1e-5,
+               rope={"q_out": qo, "k_cache": kc, "v_cache": vc, "pos": pos})
+pos_over = torch.tensor([64, 70, 1, 2], dtype=torch.int32, device="cuda")   # capacity guard
+gemm.run_fused(x, pq, x_op=3, ssq_in=ssq, ssq_tiles=H // 128, eps=1e-5,
+               rope={"q_out": qo, "k_cache": kc, "v_cache": vc, "pos": pos_over})
+pg = gemm.interleave_gate_up(gemm.PackedWeight(
+    (torch.randn((512, H), generator=g, device="cuda") / 32).half(), H, 512))
+act = torch.zeros((B, 256), dtype=torch.half, device="cuda")
+gemm.run_fused(x, pg, x_op=3, ssq_in=ssq, ssq_tiles=H // 128, eps=1e-5, silu_out=act)
+gu = torch.randn((B, 2 * H), generator=g, device="cuda").half()
+pd = gemm.PackedWeight((torch.randn((H, H), generator=g, device="cuda") / 32).half(), H, H)
+gemm.run_fused(gu, pd, x_op=2, out=torch.empty_like(x))
+x2 = x[:2].contiguous()
+gemm.run_fused(x2, gemm.permute_qkv_for_gemv(pq), x_op=3, ssq_in=ssq, ssq_tiles=1, eps=1e-5, impl="A",
+               rope={"q_out": qo[:2], "k_cache": kc[:2], "v_cache": vc[:2], "pos": pos[:2]})
+gemm.run_fused(x2, pd, out=x2, residual=x2, ssq_out=torch.zeros((H // 8, 2), device="cuda"), impl="A")
+step("fused GEMM prologues / epilogues, fused GEMV")
+
+lib = _lib.load()
+st = _lib.stream_handle()
+out = torch.empty_like(x)
+_lib.check(lib.fdpp_rmsnorm(x.data_ptr(), w_ln.data_ptr(), out.data_ptr(), B, H, 1e-5, 0, st))
+_lib.check(lib.fdpp_silu_mul(gu.data_ptr(), out.data_ptr(), B, H, 0, st))
+ids = torch.tensor([1, 5, 7, 2], dtype=torch.int32, device="cuda")
+emb = torch.randn((16, H), generator=g, device="cuda").half()
+_lib.check(lib.fdpp_embed(ids.data_ptr(), emb.data_ptr(), out.data_ptr(), B, H, ssq.data_ptr(), 0, st))
+_lib.check(lib.fdpp_row_ssq(out.data_ptr(), ssq.data_ptr(), B, H, 0, st))
+_lib.check(lib.fdpp_argmax(out.data_ptr(), ids.data_ptr(), B, H, 0, st))
+lens = pos + 1
+_lib.check(lib.fdpp_advance_positions(pos.data_ptr(), lens.data_ptr(), B, st))
+qkv = torch.randn((B, (Hq + 2 * Hkv) * 128), generator=g, device="cuda").half()
+_lib.check(lib.fdpp_rope_append(qkv.data_ptr(), qo.data_ptr(), kc.data_ptr(), vc.data_ptr(), pos.data_ptr(),
+                                B, Hq, Hkv, 128, kc.stride(0), kc.stride(1), 10000.0, 0, st))
+xs = np.random.default_rng(0).standard_normal(1000).astype(np.float32) * 3
+fd.softmax_reference(xs)
+fd.softmax_reference_f64(xs)
+fd.softmax_unified(xs, 2.0)
+fd.partial_softmax_sync(xs, 7)
+fd.sample_logits(qo, kc, 0.1, 1000, seq_lens=lens)
+step("decode glue, vector softmax, sample_logits")
+
+# ---- a tiny decode step in a CUDA graph, replayed (counters / recompute list reuse)
+cfg = llama.LlamaConfig("tiny", hidden=1024, n_heads=8, n_kv_heads=2, head_dim=128, ffn=1536,
+                        n_layers=2, vocab=512)
+table = D.DispatchTable(fingerprint="sanitize")
+for n, k_ in cfg.gemm_shapes().values():
+    table.add(D.DispatchEntry(n=n, k=k_, m1=1, m2=128))
+dec = llama.LlamaDecoder(cfg, 4, 80, table=table)
+dec.prefill_random(64, seed=3)
+dec.k_cache[0][1, 1, 10].mul_(40.0)   # force a recompute inside the graph
+dec.capture()
+for _ in range(3):
+    dec.step()
+step("decode step graph capture + 3 replays")
+print("sanitize driver done")
