@@ -251,13 +251,16 @@ def config1_attention_op(torch, fd, peak):
     out = torch.empty_like(q)
     kvs = [(torch.randn((B, H, L, Dh), generator=g, device="cuda").half(),
             torch.randn((B, H, L, Dh), generator=g, device="cuda").half()) for _ in range(8)]
-    fns = [lambda k=k, v=v: fd.decode_attention(q, k, v, cfg, "async", out=out) for k, v in kvs]
+    # as in the decode step: the preceding kernel wrote no K/V row (kv_prefetch)
+    fns = [lambda k=k, v=v: fd.decode_attention(q, k, v, cfg, "async", out=out, kv_prefetch=True)
+           for k, v in kvs]
     t = _rotating_graph_time(torch, fns)
     byt = 2 * B * H * L * Dh * 2 + 2 * B * H * Dh * 2
     return {"us": round(t * 1e6, 2), "bytes": byt, "gbs": round(byt / t / 1e9, 1),
             "frac": round(byt / t / 1e9 / peak, 3), "plan": list(fd.attention.plan(q, kvs[0][0], cfg)),
-            "launches_per_call": 2, "note": "2 launches (async + recompute check); 16.8 MB moves in "
-            "~2.6 us at HBM speed, so launch/ramp latency dominates at this size"}
+            "launches_per_call": fd.attention.launches(q, kvs[0][0], cfg),
+            "note": "one cluster launch per call (flagged rows recomputed inside the cluster); 16.8 MB "
+                    "moves in ~2.6 us at HBM speed, so launch/ramp latency dominates at this size"}
 
 
 def config2_gemm_sweep(torch, fd, D, table, peak):
@@ -398,7 +401,7 @@ def run_gpu(args):
         for li in range(dec.n_layers):
             decode_attention(dec.q, dec.k_cache[li], dec.v_cache[li], dec.attn_cfg, "async",
                              out=dec.attn, seq_lens=dec.lens, row_flags=dec.row_flags,
-                             counter=dec.recomputed)
+                             counter=dec.recomputed, kv_prefetch=True)
     t_attn = _op_graph_time(torch, attn_all, reps) / dec.n_layers
     Lnow = min(int(dec.lens[0].item()), dec.max_len)   # keys the kernel attends
     attn_bytes = B * hkv * Lnow * dh * 2 * 2 + 2 * B * hq * dh * 2

@@ -81,6 +81,12 @@ typedef struct fdpp_attn_params {
     void *workspace;          /* zero-filled before first use; kernels leave
                                  its counters zeroed on exit                   */
     size_t workspace_bytes;
+    int32_t kv_prefetch;      /* nonzero: the kernel launched just before this
+                                 call wrote no K/V row except the last one each
+                                 batch row attends (the decode step's append at
+                                 seq_lens[b] - 1), so the other rows may stream
+                                 before the programmatic-dependent-launch wait,
+                                 under the predecessor's tail; 0 = wait first */
 } fdpp_attn_params;
 
 /* Bytes of workspace `fdpp_attn_decode` needs for these params. */
@@ -90,12 +96,21 @@ fdpp_status fdpp_attn_workspace_size(const fdpp_attn_params *p, size_t *bytes);
  * p = 0 / splits_per_chunk = 0 "auto"); AttnStats arithmetic uses this p. */
 fdpp_status fdpp_attn_plan(const fdpp_attn_params *p, int32_t *chunks, int32_t *splits_per_chunk);
 
+/* Kernel launches `fdpp_attn_decode` makes for these params: 1 when the async
+ * launch joins each row group inside one thread-block cluster and recomputes
+ * its flagged rows there (the decode plans: <= 16 single-chunk CTAs per row
+ * group, no per-chunk outputs), 2 otherwise (async + recompute launch), 1 for
+ * SYNC. */
+fdpp_status fdpp_attn_launches(const fdpp_attn_params *p, int32_t *launches);
+
 /* Replaces batch_decode_attention(Q, K, V, cfg, mode) for mode in
  * {"async", "sync"} (attention.py:308-321) and the per-row recompute of
  * _batch_async (attention.py:266-286).  ASYNC: unified-phi partials, fused
  * band check, fixed-order chunk join, then the synchronized recompute of
- * flagged rows (always launched; CTAs of unflagged rows exit at once).
- * SYNC: FlashDecoding split-KV with the Eq. (2) max-rescaled join. */
+ * flagged rows: inside the same cluster launch when the row group is one
+ * cluster (see fdpp_attn_launches), else a second launch that walks the
+ * flagged (batch, kv-head) list.  SYNC: FlashDecoding split-KV with the
+ * Eq. (2) max-rescaled join. */
 fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream);
 
 /* ------------------------------------------- subsystem 2: flat GEMM family */
@@ -112,7 +127,8 @@ typedef struct fdpp_gemm_params {
                                      (may alias c)                             */
     int32_t M, N, K;
     int32_t dtype;                /* FDPP_F16 or FDPP_BF16                     */
-    int32_t block_x;              /* ImplB/C token-tile rows; 0 = auto         */
+    int32_t block_x;              /* token tile on the MMA N axis; 0 = auto
+                                     (ImplB 16/32/64, ImplC 128/256)           */
     int32_t ctas;                 /* 0 = auto: ImplB with fewer 128-row tiles
                                      than SMs uses cluster split-K (DSMEM
                                      reduction), otherwise a persistent
@@ -141,8 +157,11 @@ fdpp_status fdpp_impl_a_gemv(const fdpp_gemm_params *p, void *stream);
  * (N-tile, k-block) space with one continuous TMA/mbarrier ring per SM,
  * double-buffered TMEM accumulators, fixed-order fixup of split tiles. */
 fdpp_status fdpp_impl_b_flat(const fdpp_gemm_params *p, void *stream);
-/* ImplC (dispatch.py:117-137): conventional tcgen05 GEMM, tokens on the MMA
- * M axis (128-row tiles). */
+/* ImplC (dispatch.py:117-137): conventional big-tile tcgen05 GEMM -- all
+ * M <= 256 tokens in one 128- or 256-wide tile (weights on the MMA M axis),
+ * so each weight byte is multiplied by every token in one MMA chain rather
+ * than once per 64-token flat tile; cluster split-K while its tiles fit one
+ * wave, persistent stream-K beyond. */
 fdpp_status fdpp_impl_c_gemm(const fdpp_gemm_params *p, void *stream);
 /* run_kernel(choice, a, b) (dispatch.py:155-156). */
 fdpp_status fdpp_run_kernel(int32_t impl, const fdpp_gemm_params *p, void *stream);

@@ -35,6 +35,7 @@ class AttnParams(ctypes.Structure):
         ("row_flags", c_vp), ("viol_index", c_vp), ("rows_recomputed", c_vp),
         ("chunk_num", c_vp), ("chunk_den", c_vp),
         ("workspace", c_vp), ("workspace_bytes", c_sz),
+        ("kv_prefetch", c_i32),
     ]
 
 
@@ -68,6 +69,7 @@ SIGNATURES = {
     "fdpp_set_pdl": (ctypes.c_int, [ctypes.c_int]),
     "fdpp_attn_workspace_size": (c_i32, [ctypes.POINTER(AttnParams), ctypes.POINTER(c_sz)]),
     "fdpp_attn_plan": (c_i32, [ctypes.POINTER(AttnParams), ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
+    "fdpp_attn_launches": (c_i32, [ctypes.POINTER(AttnParams), ctypes.POINTER(c_i32)]),
     "fdpp_attn_decode": (c_i32, [ctypes.POINTER(AttnParams), c_vp]),
     "fdpp_prepack_weight": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i64, c_i32, c_vp]),
     "fdpp_gemm_workspace_size": (c_i32, [c_i32, ctypes.POINTER(GemmParams), ctypes.POINTER(c_sz)]),

@@ -156,6 +156,16 @@ def plan(q, k_cache, cfg: AttentionConfig, L: Optional[int] = None, mode: str = 
     return c.value, s.value
 
 
+def launches(q, k_cache, cfg: AttentionConfig, L: Optional[int] = None, mode: str = "async") -> int:
+    """Kernel launches one decode_attention call makes for these shapes: 1 when
+    every row group is one cluster that recomputes its own flagged rows (the
+    decode plans), else 2 (async + the flagged-list recompute launch)."""
+    prm = _params(q, k_cache, k_cache, q, cfg, mode, L)
+    n = ctypes.c_int32()
+    _lib.check(_lib.load().fdpp_attn_launches(ctypes.byref(prm), ctypes.byref(n)), "attn_launches")
+    return n.value
+
+
 def _params(q, k, v, o, cfg, mode, L):
     B, Hq, D = q.shape
     Hkv = k.shape[1]
@@ -179,7 +189,8 @@ def _params(q, k, v, o, cfg, mode, L):
 
 def decode_attention(q, k_cache, v_cache, cfg: AttentionConfig, mode: str = "async", *,
                      out=None, L: Optional[int] = None, seq_lens=None, row_flags=None,
-                     viol_index=None, chunk_num=None, chunk_den=None, counter=None, stream=None):
+                     viol_index=None, chunk_num=None, chunk_den=None, counter=None, stream=None,
+                     kv_prefetch: bool = False):
     """Batched decode attention on CUDA tensors.
 
     q [B, Hq, D]; k_cache / v_cache [B, Hkv, Lmax, D] (key rows contiguous);
@@ -187,7 +198,9 @@ def decode_attention(q, k_cache, v_cache, cfg: AttentionConfig, mode: str = "asy
     batch row b when an int32 device tensor is given (read at run time).
     Returns (out [B, Hq, D], AttnStats).  Capturable into CUDA graphs when
     ``out`` / ``row_flags`` / ``counter`` are preallocated (no allocation, no
-    host sync).
+    host sync).  ``kv_prefetch``: the kernel launched just before wrote no K/V
+    row except each batch row's last attended one (a decode step's append), so
+    the rest may stream before the programmatic-dependent-launch wait.
     """
     torch = _torch()
     if mode not in ("sync", "async"):
@@ -222,6 +235,7 @@ def decode_attention(q, k_cache, v_cache, cfg: AttentionConfig, mode: str = "asy
     prm.rows_recomputed = counter.data_ptr() if counter is not None else None
     prm.chunk_num = chunk_num.data_ptr() if chunk_num is not None else None
     prm.chunk_den = chunk_den.data_ptr() if chunk_den is not None else None
+    prm.kv_prefetch = 1 if kv_prefetch else 0
     lib = _lib.load()
     need = ctypes.c_size_t()
     _lib.check(lib.fdpp_attn_workspace_size(ctypes.byref(prm), ctypes.byref(need)), "attention")

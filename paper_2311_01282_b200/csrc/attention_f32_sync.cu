@@ -1,0 +1,6 @@
+// Subsystem 1 kernels, f32 sync softmax: explicit instantiations (attention_kernels.cuh).
+#include "attention_kernels.cuh"
+
+namespace fdpp {
+template fdpp_status by_d<float, false>(const AttnArgs &, int, int, int, cudaStream_t);
+}  // namespace fdpp

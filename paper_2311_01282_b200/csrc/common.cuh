@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <utility>
 
@@ -37,6 +38,24 @@ fdpp_status run_gemm_f32(int impl, const fdpp_gemm_params *p, cudaStream_t st);
     } while (0)
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// Per-device "done" bits for one-time launch setup (cudaFuncSetAttribute):
+// thread-safe (the setup is idempotent, so two threads racing both run it)
+// and per device (a second GPU in the process gets its own setup).
+struct DeviceOnce {
+    std::atomic<uint64_t> done{0};
+    template <typename F>
+    cudaError_t run(F &&f) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        const uint64_t bit = 1ull << (dev & 63);
+        if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+        e = f();
+        if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+        return e;
+    }
+};
 
 // Every workspace starts with a fixed region of ticket counters that is never
 // used for anything else, so a pooled buffer reused by a differently shaped
@@ -317,6 +336,16 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// split form: arrive (non-blocking) now, wait later (every thread does both)
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
+    return *reinterpret_cast<const volatile uint32_t *>(p);
+}
 // address of `local_smem` in the shared memory of cluster CTA `rank`
 __device__ __forceinline__ uint32_t dsmem_map(const void *local_smem, uint32_t rank) {
     uint32_t r;
@@ -337,6 +366,10 @@ __device__ __forceinline__ float4 dsmem_ld_v4(uint32_t cluster_addr) {
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "r"(cluster_addr));
     return v;
+}
+// OR into a 32-bit word in a cluster peer's shared memory
+__device__ __forceinline__ void dsmem_red_or_u32(uint32_t cluster_addr, uint32_t v) {
+    asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t dsmem_map_addr(uint32_t local_addr, uint32_t rank) {
     uint32_t r;

@@ -12,8 +12,12 @@
 //                             a padded copy), multi-stage TMA/mbarrier ring (the
 //                             paper's double buffer generalised to S stages),
 //                             N-split grid plus deterministic split-K.
-//   ImplC  gemm_tc<SWAP=0>    conventional GEMM (dispatch.py:95-137): tokens on
-//                             the MMA M axis (128-row tiles), weights on N.
+//   ImplC  conventional GEMM (dispatch.py:95-137): the big-tile schedule --
+//                             all M <= 256 tokens in one 128- or 256-wide MMA N
+//                             tile (weights on the 128-row MMA M axis), so each
+//                             weight byte meets every token in one MMA chain
+//                             instead of once per 64-token flat tile; same
+//                             cluster split-K / stream-K grids, deeper ring.
 //
 // All paths: C[M,N] = A[M,K] · W[N,K]^T (+ R), W = prepacked reference B[K,N].
 #include <cstring>
@@ -787,7 +791,9 @@ struct ClSmem {
     // fp32 partial in 4-column groups, [BX/4][128 rows][4]: a warp's 16-B
     // accesses of one group cover 512 contiguous bytes (local and DSMEM)
     static constexpr uint32_t PART = BX * 128 * 4;
-    static constexpr uint32_t BAR_OFF = RING > 2 * PART ? RING : 2 * PART;  // + RoPE staging
+    // the fused epilogues (flat tiles, BX <= 64) stage RoPE / SiLU values after the partial
+    static constexpr uint32_t STAGED = BX <= 64 ? 2 * PART : PART;
+    static constexpr uint32_t BAR_OFF = RING > STAGED ? RING : STAGED;
     static constexpr uint32_t TOTAL = BAR_OFF + (3 * STAGES + 4) * 8 + 16 + 1024;
 };
 
@@ -832,40 +838,46 @@ __device__ __forceinline__ void cl_store_col(const ClEpi<T> &e, int c, float o, 
 
 template <typename T, int MMA_N, int CS>
 __device__ __forceinline__ void cl_reduce_store(const ClEpi<T> &e) {
-    constexpr int PER = (((MMA_N + CS - 1) / CS) + 3) & ~3;
-    constexpr int NG = PER / 4;
+    constexpr int PER = (((MMA_N + CS - 1) / CS) + 3) & ~3;  // this rank's columns
+    // columns per round trip: every DSMEM load of a chunk in flight at once,
+    // <= 16 float4 of loads in registers
+    constexpr int NG = (PER / 4) < (16 / CS) ? (PER / 4) : (16 / CS);
+    constexpr int CH = 4 * NG;
     const int n = e.n0 + e.row;
-    const uint32_t base = smem_u32(e.part) + (uint32_t)(((e.c_beg >> 2) * 128 + e.row) * 16);
-    float4 buf[NG][CS];
-    float rv[PER];
+#pragma unroll 1
+    for (int cb = e.c_beg; cb < e.c_end; cb += CH) {
+        const uint32_t base = smem_u32(e.part) + (uint32_t)(((cb >> 2) * 128 + e.row) * 16);
+        float4 buf[NG][CS];
+        float rv[CH];
 #pragma unroll
-    for (int g = 0; g < NG; ++g) {
-        const bool live = e.c_beg + 4 * g < e.c_end && e.m0 + e.c_beg + 4 * g < e.M;
+        for (int g = 0; g < NG; ++g) {
+            const bool live = cb + 4 * g < e.c_end && e.m0 + cb + 4 * g < e.M;
 #pragma unroll
-        for (int q = 0; q < CS; ++q)
-            buf[g][q] = live ? dsmem_ld_v4(dsmem_map_addr(base + 2048u * g, q))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        const int m = e.m0 + e.c_beg + j;
-        rv[j] = (e.R && e.c_beg + j < e.c_end && m < e.M && n < e.N)
-                    ? Elem<T>::to_f(e.R[(int64_t)m * e.ldr + n])
-                    : 0.f;
-    }
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-        if (e.c_beg + 4 * g >= e.c_end) break;
-        float o[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int q = 0; q < CS; ++q) {  // rank order
-            o[0] += buf[g][q].x;
-            o[1] += buf[g][q].y;
-            o[2] += buf[g][q].z;
-            o[3] += buf[g][q].w;
+            for (int q = 0; q < CS; ++q)
+                buf[g][q] = live ? dsmem_ld_v4(dsmem_map_addr(base + 2048u * g, q))
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cl_store_col<T, MMA_N>(e, e.c_beg + 4 * g + j, o[j], rv[4 * g + j]);
+        for (int j = 0; j < CH; ++j) {
+            const int m = e.m0 + cb + j;
+            rv[j] = (e.R && cb + j < e.c_end && m < e.M && n < e.N)
+                        ? Elem<T>::to_f(e.R[(int64_t)m * e.ldr + n])
+                        : 0.f;
+        }
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
+            if (cb + 4 * g >= e.c_end) break;
+            float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int q = 0; q < CS; ++q) {  // rank order
+                o[0] += buf[g][q].x;
+                o[1] += buf[g][q].y;
+                o[2] += buf[g][q].z;
+                o[3] += buf[g][q].w;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) cl_store_col<T, MMA_N>(e, cb + 4 * g + j, o[j], rv[4 * g + j]);
+        }
     }
 }
 
@@ -909,7 +921,7 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     using S = TcSmem<BW, BX, STAGES, XF>;
     using CS = ClSmem<BX, STAGES, XF>;
     constexpr int MMA_N = BX;
-    constexpr uint32_t TMEM_COLS = MMA_N <= 32 ? 32 : MMA_N <= 64 ? 64 : 128;
+    constexpr uint32_t TMEM_COLS = MMA_N <= 32 ? 32 : MMA_N <= 64 ? 64 : MMA_N <= 128 ? 128 : 256;
     constexpr uint32_t IDESC = umma_idesc_f16(128, MMA_N, std::is_same<T, __nv_bfloat16>::value);
 
     extern __shared__ uint8_t smem_raw[];
@@ -1019,6 +1031,7 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         ClEpi<T> ep{part, rbuf, C, ldc, R, ldr, M, N, n0, m0, c_beg, c_end, row, lane, quad, rope || silu,
                     fz.x_op == 3 ? s_inv_rms : nullptr, fz.ssq_out ? &s_ssq[0][0] : nullptr};
         switch (ck.cs) {
+            case 1: cl_reduce_store<T, MMA_N, 1>(ep); break;
             case 2: cl_reduce_store<T, MMA_N, 2>(ep); break;
             case 4: cl_reduce_store<T, MMA_N, 4>(ep); break;
             case 8: cl_reduce_store<T, MMA_N, 8>(ep); break;
@@ -1164,21 +1177,29 @@ struct TcPlan {
     TcCluster ck;
 };
 
-static int pick_block_x(int M, bool swap) {
-    if (!swap) return 128;
+// Token tile on the MMA N axis.  ImplB (the flat GEMM) pads M to 16 / 32 / 64
+// and loops over 64-token tiles beyond that; ImplC (the conventional GEMM)
+// takes all of M <= 256 in one 128- or 256-wide tile, so every weight byte
+// meets every token in one MMA chain (256-token tiles beyond).
+static int pick_block_x(int M, bool flat) {
+    if (!flat) return M <= 128 ? 128 : 256;
     if (M <= 16) return 16;
     if (M <= 32) return 32;
     return 64;
 }
 
-static fdpp_status plan_tc(const fdpp_gemm_params *p, bool swap, TcPlan *pl) {
+// CTAs of a tile kernel that fit on one SM: the 256-token tile's ~190 KB ring
+// takes a whole SM; every other tile runs two per SM.
+static int ctas_per_sm(int bx) { return bx >= 256 ? 1 : 2; }
+
+static fdpp_status plan_tc(const fdpp_gemm_params *p, bool flat, TcPlan *pl) {
     const int kb_total = ceil_div(p->K, TC_BK);
-    pl->bx = p->block_x > 0 ? p->block_x : pick_block_x(p->M, swap);
-    if (swap) {
+    pl->bx = p->block_x > 0 ? p->block_x : pick_block_x(p->M, flat);
+    if (flat) {
         FDPP_REQUIRE(pl->bx == 16 || pl->bx == 32 || pl->bx == 64, FDPP_ERR_VALUE,
                      "ImplB block_x must be 16, 32 or 64");
     } else {
-        FDPP_REQUIRE(pl->bx == 128, FDPP_ERR_VALUE, "ImplC block_x must be 128");
+        FDPP_REQUIRE(pl->bx == 128 || pl->bx == 256, FDPP_ERR_VALUE, "ImplC block_x must be 128 or 256");
     }
     pl->bw = 128;
     TcWork &w = pl->wk;
@@ -1189,18 +1210,19 @@ static fdpp_status plan_tc(const fdpp_gemm_params *p, bool swap, TcPlan *pl) {
     FDPP_REQUIRE(total < (1ll << 31), FDPP_ERR_SHAPE, "GEMM too large");
     const int sms = sm_count() > 0 ? sm_count() : 148;
     const int tiles = w.n_tiles_n * w.n_tiles_m;
-    // Auto policy for ImplB (measured in-graph on B200 across the Llama shapes,
+    // Auto policy (measured in-graph on B200 across the Llama shapes,
     // tools/cs_sweep.py, profiles/r1_gemm_modes.txt): cluster split-K with 8
     // CTAs per tile for <= 40 tiles (e.g. N = 4096), 2 per tile up to ~0.9 SMs
     // of tiles (N = 12288), one CTA per tile while every tile fits in one wave
-    // at two CTAs per SM (N = 22016, 32000); beyond that, stream-K with two
-    // CTAs per SM.  ctas < 0 forces cs = -ctas.
-    pl->cluster = swap && ((p->ctas == 0 && tiles <= 2 * sms) || p->ctas < 0);
+    // (N = 22016, 32000); beyond that, persistent stream-K.  ctas < 0 forces
+    // cs = -ctas.  The wave is 2 CTAs per SM, 1 for ImplC's 256-token tiles.
+    const int slots = ctas_per_sm(pl->bx) * sms;
+    pl->cluster = (p->ctas == 0 && tiles <= slots) || p->ctas < 0;
     if (pl->cluster) {
-        // the largest power-of-two split that keeps every CTA in one wave at two
-        // per SM (the 7B shapes: 8 / 2 / 1 as measured; the 70B shards get 4-16)
+        // the largest power-of-two split that keeps every CTA in one wave
+        // (the 7B shapes: 8 / 2 / 1 as measured; the 70B shards get 4-16)
         int cs = 1;
-        while (cs < 16 && tiles * cs * 2 <= 2 * sms && kb_total / (cs * 2) >= 2) cs *= 2;
+        while (cs < 16 && tiles * cs * 2 <= slots && kb_total / (cs * 2) >= 2) cs *= 2;
         if (p->ctas < 0) cs = -p->ctas;
         cs = cs < 1 ? 1 : (cs > 16 ? 16 : cs);  // > 8: non-portable cluster size
         if (cs > kb_total) cs = kb_total;
@@ -1215,7 +1237,7 @@ static fdpp_status plan_tc(const fdpp_gemm_params *p, bool swap, TcPlan *pl) {
     }
     // persistent stream-K grid: one CTA per SM (or the `ctas` override),
     // contiguous equal unit ranges -- perfect balance up to one k-block
-    int ctas = p->ctas > 0 ? p->ctas : (swap ? 2 * sms : sms);
+    int ctas = p->ctas > 0 ? p->ctas : slots;
     if (ctas > total) ctas = (int)total;
     w.units = (int)((total + ctas - 1) / ctas);
     pl->grid = (int)((total + w.units - 1) / w.units);
@@ -1249,19 +1271,17 @@ static fdpp_status launch_cluster(const fdpp_gemm_params *p, const TcPlan &pl, c
                                   cudaStream_t st) {
     using S = ClSmem<BX, STAGES, XF>;
     auto kern = gemm_cluster_kernel<T, BX, STAGES, XF>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)S::TOTAL);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+    static DeviceOnce attr;  // per instantiation and device
+    cudaError_t e = attr.run([&] {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::TOTAL);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_cluster)");
-        attr_set = true;
-    }
-    cudaError_t e = launch_kernel_cluster(
+        if (r == cudaSuccess) r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        return r;
+    });
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_cluster)");
+    e = launch_kernel_cluster(
         kern, dim3(pl.grid, pl.wk.n_tiles_m), dim3(XF ? TC_THREADS_XF : TC_THREADS), S::TOTAL, st,
         pl.ck.cs, L.mw, L.mx, L.mu, static_cast<T *>(p->c), p->ldc, static_cast<const T *>(p->r),
         p->ldr, p->M, p->N, p->K, pl.ck, L.fz);
@@ -1277,23 +1297,22 @@ static fdpp_status launch_tc(const fdpp_gemm_params *p, const TcPlan &pl, const 
     }
     using S = TcSmem<BW, BX, STAGES, XF>;
     auto kern = gemm_tc_kernel<T, BW, BX, SWAP, STAGES, XF>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)S::TOTAL);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+    static DeviceOnce attr;  // per instantiation and device
+    cudaError_t e = attr.run([&] {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::TOTAL);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_tc)");
-        attr_set = true;
-    }
+        return r;
+    });
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_tc)");
     int *counters = nullptr;
     float *ws = nullptr;
     if (has_split_tiles(pl)) {
         counters = static_cast<int *>(p->workspace);
         ws = reinterpret_cast<float *>(static_cast<char *>(p->workspace) + kWsCounterBytes);
     }
-    cudaError_t e = launch_kernel(kern, dim3(pl.grid), dim3(XF ? TC_THREADS_XF : TC_THREADS),
+    e = launch_kernel(kern, dim3(pl.grid), dim3(XF ? TC_THREADS_XF : TC_THREADS),
                                   S::TOTAL, st, L.mw, L.mx, L.mu, static_cast<T *>(p->c), p->ldc,
                                   static_cast<const T *>(p->r), p->ldr, p->M, p->N, p->K, pl.wk, ws,
                                   counters, L.fz);
@@ -1308,23 +1327,27 @@ static fdpp_status dispatch_stages(const fdpp_gemm_params *p, const TcPlan &pl, 
     constexpr int BW = 128;
     // default ring: ~100 KB of stages (>= 4x the ~20 KB/SM Little's-law need
     // at 6.5 TB/s), small enough that the next kernel's CTA fits beside it on
-    // the SM while this one drains (PDL overlap)
-    constexpr int DEEP = (100 * 1024) / ((BW + BX) * TC_BK * 2) < 4
-                             ? 4
-                             : (100 * 1024) / ((BW + BX) * TC_BK * 2);
+    // the SM while this one drains (PDL overlap).  Conventional tiles: 3 x 32 KB
+    // (128 tokens, two CTAs per SM) or 4 x 48 KB (256 tokens, one per SM).
+    constexpr int STAGE = (BW + BX) * TC_BK * 2;
+    constexpr int DEEP = BX >= 256 ? 4 : BX >= 128 ? 3 : ((100 * 1024) / STAGE < 4 ? 4 : (100 * 1024) / STAGE);
     constexpr int DEEP_XF = (100 * 1024) / ((BW + 2 * BX) * TC_BK * 2) < 4
                                 ? 4
                                 : (100 * 1024) / ((BW + 2 * BX) * TC_BK * 2);
-    if (L.xf) {
-        if constexpr (SWAP) return launch_tc<T, BW, BX, SWAP, DEEP_XF, true>(p, pl, L, st);
-        set_error("fused activation transforms need ImplB");
-        return FDPP_ERR_UNSUPPORTED;
-    }
+    if constexpr (BX >= 128) {  // ImplC: the deep ring, no fused prologue
+        if (L.xf) {
+            set_error("fused activation transforms need ImplB");
+            return FDPP_ERR_UNSUPPORTED;
+        }
+        return launch_tc<T, BW, BX, SWAP, DEEP, false>(p, pl, L, st);
+    } else {
+    if (L.xf) return launch_tc<T, BW, BX, SWAP, DEEP_XF, true>(p, pl, L, st);
     switch (pl.stages) {
         case 1: return launch_tc<T, BW, BX, SWAP, 1, false>(p, pl, L, st);
         case 2: return launch_tc<T, BW, BX, SWAP, 2, false>(p, pl, L, st);
         case 4: return launch_tc<T, BW, BX, SWAP, 4, false>(p, pl, L, st);
         default: return launch_tc<T, BW, BX, SWAP, DEEP, false>(p, pl, L, st);
+    }
     }
 }
 
@@ -1350,7 +1373,9 @@ static int l2_prefetch_blocks() {
     return v;
 }
 
-static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st,
+// flat = ImplB (16/32/64-token tiles), else ImplC (128/256-token tiles); both
+// put the weight rows on the MMA M axis (swap-AB).
+static fdpp_status run_tc(const fdpp_gemm_params *p, bool flat, cudaStream_t st,
                           const fdpp_gemm_fuse *fuse = nullptr) {
     const bool epi_fuse = fuse && (fuse->ssq_out || fuse->q_out || fuse->act_out);
     fdpp_status s = check_gemm(p, fuse && (fuse->q_out || fuse->act_out));
@@ -1360,11 +1385,12 @@ static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st,
     if (epi_fuse && q.ctas >= 0) {  // fused epilogues live in the cluster split-K kernel
         q.ctas = 0;
         TcPlan probe;
-        if ((s = plan_tc(&q, swap, &probe)) != FDPP_OK) return s;
+        if ((s = plan_tc(&q, flat, &probe)) != FDPP_OK) return s;
         if (!probe.cluster) q.ctas = -2;
     }
-    if ((s = plan_tc(&q, swap, &pl)) != FDPP_OK) return s;
+    if ((s = plan_tc(&q, flat, &pl)) != FDPP_OK) return s;
     FDPP_REQUIRE(!epi_fuse || pl.cluster, FDPP_ERR_UNSUPPORTED, "fused epilogue needs cluster mode");
+    FDPP_REQUIRE(!fuse || flat, FDPP_ERR_UNSUPPORTED, "fused prologues / epilogues run on ImplB tiles");
     FDPP_REQUIRE(tc_workspace(pl, p) <= p->workspace_bytes, FDPP_ERR_WORKSPACE,
                  "GEMM workspace too small: need %zu bytes", tc_workspace(pl, p));
     TcLaunch L;
@@ -1412,18 +1438,18 @@ static fdpp_status run_tc(const fdpp_gemm_params *p, bool swap, cudaStream_t st,
         if ((s = make_kmajor_map(&L.mu, up, p->M, p->K, p->lda, pl.bx, p->dtype)) != FDPP_OK) return s;
     }
     const bool bf = p->dtype == FDPP_BF16;
-    if (swap) {
-        switch (pl.bx) {
-            case 16: return bf ? dispatch_stages<__nv_bfloat16, 16, true>(&q, pl, L, st)
-                               : dispatch_stages<__half, 16, true>(&q, pl, L, st);
-            case 32: return bf ? dispatch_stages<__nv_bfloat16, 32, true>(&q, pl, L, st)
-                               : dispatch_stages<__half, 32, true>(&q, pl, L, st);
-            default: return bf ? dispatch_stages<__nv_bfloat16, 64, true>(&q, pl, L, st)
-                               : dispatch_stages<__half, 64, true>(&q, pl, L, st);
-        }
+    switch (pl.bx) {
+        case 16: return bf ? dispatch_stages<__nv_bfloat16, 16, true>(&q, pl, L, st)
+                           : dispatch_stages<__half, 16, true>(&q, pl, L, st);
+        case 32: return bf ? dispatch_stages<__nv_bfloat16, 32, true>(&q, pl, L, st)
+                           : dispatch_stages<__half, 32, true>(&q, pl, L, st);
+        case 64: return bf ? dispatch_stages<__nv_bfloat16, 64, true>(&q, pl, L, st)
+                           : dispatch_stages<__half, 64, true>(&q, pl, L, st);
+        case 128: return bf ? dispatch_stages<__nv_bfloat16, 128, true>(&q, pl, L, st)
+                            : dispatch_stages<__half, 128, true>(&q, pl, L, st);
+        default: return bf ? dispatch_stages<__nv_bfloat16, 256, true>(&q, pl, L, st)
+                           : dispatch_stages<__half, 256, true>(&q, pl, L, st);
     }
-    return bf ? dispatch_stages<__nv_bfloat16, 128, false>(&q, pl, L, st)
-              : dispatch_stages<__half, 128, false>(&q, pl, L, st);
 }
 
 template <typename T>

@@ -223,10 +223,20 @@ class LlamaDecoder:
                     L["gate_up_f"] = interleave_gate_up(fold_norm(L.pop("gate_up"), L["ln2"]))
             self.lm_head_f = fold_norm(self.lm_head, self.ln_f)
         self.fused = fused
-        # fused: embed + L x (qkv+rope, attn async, attn recompute, o, gate_up+silu, down
-        #        [+ 2 row-ssq after the all-reduces]) + lm_head + argmax + advance
-        per_layer = 6 + (2 if tp_size > 1 else 0)
-        self.launches_per_step = (1 + self.n_layers * per_layer + 3) if fused else (1 + self.n_layers * 10 + 4)
+        self._tp_size = tp_size
+
+    @property
+    def launches_per_step(self) -> int:
+        """Kernels one decode step launches: embed + L x (qkv+rope, attention (1
+        launch when the cluster recomputes its own flagged rows, else 2), o,
+        gate_up+silu, down [+ 2 row-ssq after the all-reduces]) + lm_head +
+        argmax + advance (unfused: 8 + attention per layer, + 4)."""
+        from .attention import launches
+        na = launches(self.q, self.k_cache[0], self.attn_cfg, mode="async")
+        if self.fused:
+            per_layer = 4 + na + (2 if self._tp_size > 1 else 0)
+            return 1 + self.n_layers * per_layer + 3
+        return 1 + self.n_layers * (8 + na) + 4
 
     # ------------------------------------------------------------------ calibration
     def calibrate(self, target_coverage: float = 0.9999, margin: float = 1.0, samples_per_layer: int = 65536,
@@ -337,8 +347,10 @@ class LlamaDecoder:
                             "theta": cfg.rope_theta})
             if self._layer_hook is not None:
                 self._layer_hook(li)
+            # the QKV epilogue / rope_append just wrote only row pos of the caches
             decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
-                             seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed)
+                             seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed,
+                             kv_prefetch=True)
             run_fused(self.attn.view(B, Hq * Dh), L["o"], out=self.x, residual=self.x if lead else None,
                       ssq_out=None if tp or impl == "A" else self.ssq_b, ws_tag="decode_gemm", impl=impl)
             if tp:
@@ -375,8 +387,10 @@ class LlamaDecoder:
                        "rope_append")
             if self._layer_hook is not None:
                 self._layer_hook(li)
+            # the QKV epilogue / rope_append just wrote only row pos of the caches
             decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
-                             seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed)
+                             seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed,
+                             kv_prefetch=True)
             self._gemm("o", self.attn.view(B, Hq * Dh), L["o"], self.x, residual=self.x)
             _lib.check(lib.fdpp_rmsnorm(self.x.data_ptr(), L["ln2"].data_ptr(), self.h.data_ptr(), B,
                                         cfg.hidden, cfg.eps, dt, st), "rmsnorm")

@@ -281,3 +281,74 @@ def test_ragged_seq_lens(fd, torch, Hkv, p):
             ref = O.attention_reference(qn[b, h][None], kn[b, h // G, :n], vn[b, h // G, :n], cfg.scale)
             assert fd.rel_error_rowwise(o[b, h][None].float().cpu().numpy(), ref) <= TOL
     assert st.rows_recomputed == 0
+
+
+def test_incluster_recompute_matches_two_launch(tmp_path):
+    """The decode plans recompute flagged rows inside the async launch's cluster
+    (one launch).  FDPP_ATTN_INCLUSTER=0 restores the separate list-walking
+    recompute launch; FDPP_ATTN_ABORT=0 keeps streaming after a violation.
+    * in-cluster, no early stop: the same arithmetic in the same order as the
+      two-launch form -- outputs, flag sets and counters bitwise equal;
+    * in-cluster with the early stop (default): a group that saw a violation
+      stops its async stream and is recomputed whole, its flags re-derived
+      from the sync pass's band check -- flag sets and counters still equal
+      bitwise, outputs within the fp16 bar (its unflagged rows now come from
+      the sync softmax) and bitwise on every group without a flagged row."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mode, env_over in (("two", {"FDPP_ATTN_INCLUSTER": "0"}),
+                           ("one", {"FDPP_ATTN_INCLUSTER": "1", "FDPP_ATTN_ABORT": "0"}),
+                           ("abort", {"FDPP_ATTN_INCLUSTER": "1", "FDPP_ATTN_ABORT": "1"})):
+        path = str(tmp_path / f"inc_{mode}.npz")
+        env = dict(os.environ, **env_over)
+        subprocess.run([sys.executable, os.path.join(root, "tests", "helpers", "attn_dump.py"), path],
+                       check=True, env=env, cwd=root, timeout=600)
+        res[mode] = np.load(path)
+    two, one, ab = res["two"], res["one"], res["abort"]
+    for key in two.files:
+        if key.startswith("n"):
+            assert two[key][0] == one[key][0] == ab[key][0] and two[key][0] > 0, key   # rows recomputed
+            assert (two[key][1], one[key][1], ab[key][1]) == (2, 1, 1), key           # launches per call
+        elif key.startswith("f"):
+            assert np.array_equal(two[key], one[key]) and np.array_equal(two[key], ab[key]), key
+        else:
+            assert np.array_equal(two[key], one[key]), key
+            o2, oa = two[key].astype(np.float32), ab[key].astype(np.float32)
+            D = o2.shape[-1]
+            assert fd_rel(oa.reshape(-1, D), o2.reshape(-1, D)) <= TOL, key
+            # bitwise on the (b, kv-head) groups without a flagged row
+            flags = two["f" + key[1:]]
+            B, Hq = flags.shape
+            i = int(key[1:])
+            Hkv = __import__("tests.helpers.attn_dump", fromlist=["CASES"]).CASES[i][2]
+            G = Hq // Hkv
+            clean = ~flags.reshape(B, Hkv, G).any(-1)
+            assert np.array_equal(o2.reshape(B, Hkv, G, D)[clean], oa.reshape(B, Hkv, G, D)[clean]), key
+
+
+def fd_rel(a, b):
+    return float((np.abs(a - b).max(1) / np.maximum(np.abs(b).max(1), 1e-8)).max())
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,L", [(1, 32, 32, 1024), (2, 32, 2, 1500)])
+def test_incluster_recompute_vs_oracle(fd, torch, B, Hq, Hkv, L):
+    # the single-launch recompute (auto plan, cluster join) against the oracle,
+    # with one key far outside the band in two (b, kv-head) groups
+    q, k, v = _qkv(torch, B, Hq, Hkv, L, 128, 17, torch.float16)
+    groups = [(0, 0), (B - 1, Hkv - 1)]
+    for b, h in groups:
+        k[b, h, L // 2].mul_(40.0)
+    calib = fd.ScalingCalibration(*GOLD_CAL, coverage=1.0)
+    cfg = fd.AttentionConfig.auto(1 / math.sqrt(128), calib)
+    assert fd.attention.launches(q, k, cfg) == 1
+    p, _ = fd.attention.plan(q, k, cfg)
+    o, st = fd.decode_attention(q, k, v, cfg, "async")
+    ref, redo, clear = _oracle_batched(q, k, v, p, cfg.scale, O.Calib(*GOLD_CAL))
+    assert clear.all()
+    assert np.array_equal(st.row_mask.cpu().numpy(), redo)
+    G = Hq // Hkv
+    assert st.rows_recomputed == int(redo.sum())
+    assert any(redo[b, h * G:(h + 1) * G].any() for b, h in groups)
+    assert fd.rel_error_rowwise(o.float().cpu().numpy().reshape(-1, 128), ref.reshape(-1, 128)) <= TOL

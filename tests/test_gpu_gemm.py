@@ -93,6 +93,24 @@ def test_llama_shapes_all_impls(fd, torch, N, K, M):
     assert max(errs.values()) <= TOL, errs
 
 
+@pytest.mark.parametrize("N,K,M", [(12288, 4096, 128), (4096, 4096, 256), (4096, 11008, 96),
+                                   (11008, 4096, 200), (22016, 4096, 256)])
+def test_conventional_regime(fd, torch, N, K, M):
+    """M beyond the flat band (the reference's sweep reaches 256, dispatch.py:24):
+    ImplB (token tiles of 64) and ImplC (tokens on the MMA M axis; cluster
+    split-K while its tiles fit one wave, stream-K beyond) against the oracle."""
+    a, b = _operands(torch, M, N, K, 7 * M + N, torch.float16)
+    pw = fd.pack_weight(b)
+    ref = _oracle(a, b)
+    D = __import__("importlib").import_module("paper_2311_01282_b200.dispatch")
+    errs = {}
+    for ch in (D.KernelChoice.IMPL_B, D.KernelChoice.IMPL_C):
+        out = D.run_device(ch, a, pw)
+        errs[ch.value] = fd.rel_error_rowwise(out.float().cpu().numpy(), ref)
+        assert torch.equal(out, D.run_device(ch, a, pw))   # bitwise rerun
+    assert max(errs.values()) <= TOL, errs
+
+
 def test_bf16(fd, torch):
     a, b = _operands(torch, 16, 4096, 4096, 5, torch.bfloat16)
     ref = _oracle(a, b)

@@ -27,6 +27,10 @@ from paper_2311_01282_b200 import _lib, gemm, llama  # noqa: E402
 
 D = importlib.import_module("paper_2311_01282_b200.dispatch")
 torch.cuda.set_device(0)
+if os.environ.get("SANITIZE_NOPDL") == "1":
+    # initcheck does not follow writes made by a programmatic-dependent
+    # predecessor; run the same launches in plain stream order
+    _lib.load().fdpp_set_pdl(0)
 g = torch.Generator(device="cuda").manual_seed(0)
 cal = fd.ScalingCalibration(phi=-7.775933742523193, a=-1.0, b=16.577659606933594, coverage=1.0)
 
