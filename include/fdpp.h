@@ -45,6 +45,8 @@ int fdpp_sm_count(void);
 int fdpp_set_pdl(int enable);
 
 /* ------------------------------------------------- subsystem 1: attention */
+#define FDPP_AR_MAX_WORLD 8
+
 typedef enum { FDPP_ATTN_ASYNC = 0, FDPP_ATTN_SYNC = 1 } fdpp_attn_mode;
 
 /* Split-KV decode/prefill attention over a [B, Hkv, L, D] cache.  Query head
@@ -195,7 +197,33 @@ typedef struct fdpp_gemm_fuse {
                                 gate rows then the matching 64 up rows): act_out[m, 64 t + j]
                                 = silu(gate) * up, [M, N/2] with leading dim act_ld; C unused */
     int64_t act_ld;
+    int32_t ar_rank, ar_world;  /* optional one-shot all-reduce of C over ar_world >= 2
+                                tensor-parallel ranks (row-parallel O / down projections):
+                                every rank runs this call on its K shard with the same M, N,
+                                K; each CTA pushes its fp32 output slice into every peer's
+                                receive buffer over peer memory, publishes an epoch flag,
+                                waits for the peers' slices and writes C = sum over ranks in
+                                rank order + r (residual added once; ssq_out covers the
+                                reduced C).  Replaces partial GEMM + ncclAllReduce.         */
+    int64_t ar_cap;          /* floats per receive slot (>= M * N), as sized for
+                                fdpp_ar_workspace_size                                      */
+    void *ar_ws[FDPP_AR_MAX_WORLD]; /* each rank's all-reduce workspace, mapped in this
+                                process (its own from fdpp_ar_alloc, peers' from
+                                fdpp_ipc_open), zero-filled before first use               */
 } fdpp_gemm_fuse;
+
+/* Peer-memory all-reduce workspace: bytes for `world` ranks and `cap` floats per
+ * receive slot; allocation (cudaMalloc, zero-filled) and CUDA IPC export/import so
+ * each rank can map its peers' workspaces (handles are 64 bytes). */
+fdpp_status fdpp_ar_workspace_size(int32_t world, int64_t cap, size_t *bytes);
+fdpp_status fdpp_ar_alloc(size_t bytes, void **ptr);
+fdpp_status fdpp_ar_free(void *ptr);
+fdpp_status fdpp_ipc_get_handle(void *ptr, void *handle64);
+fdpp_status fdpp_ipc_open(const void *handle64, void **ptr);
+fdpp_status fdpp_ipc_close(void *ptr);
+/* 1 in *timed_out if a fused all-reduce on this workspace gave up waiting for a
+ * peer (~1 s), else 0; synchronises the device. */
+fdpp_status fdpp_ar_check(const void *ws, int32_t *timed_out);
 
 /* ImplB with the fusions above (fused epilogues run in cluster split-K mode). */
 fdpp_status fdpp_gemm_fused(const fdpp_gemm_params *p, const fdpp_gemm_fuse *fuse, void *stream);

@@ -21,6 +21,9 @@ IMPL_A, IMPL_B, IMPL_C = 0, 1, 2
 c_i32, c_i64, c_f32, c_vp, c_sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t
 
 
+AR_MAX_WORLD = 8  # FDPP_AR_MAX_WORLD
+
+
 class AttnParams(ctypes.Structure):
     """fdpp_attn_params (include/fdpp.h)."""
     _fields_ = [
@@ -58,6 +61,7 @@ class GemmFuse(ctypes.Structure):
         ("q_out", c_vp), ("k_cache", c_vp), ("v_cache", c_vp), ("pos", c_vp),
         ("Hq", c_i32), ("Hkv", c_i32), ("cache_stride_b", c_i64), ("cache_stride_h", c_i64),
         ("theta", c_f32), ("act_out", c_vp), ("act_ld", c_i64),
+        ("ar_rank", c_i32), ("ar_world", c_i32), ("ar_cap", c_i64), ("ar_ws", c_vp * AR_MAX_WORLD),
     ]
 
 
@@ -70,6 +74,13 @@ SIGNATURES = {
     "fdpp_attn_workspace_size": (c_i32, [ctypes.POINTER(AttnParams), ctypes.POINTER(c_sz)]),
     "fdpp_attn_plan": (c_i32, [ctypes.POINTER(AttnParams), ctypes.POINTER(c_i32), ctypes.POINTER(c_i32)]),
     "fdpp_attn_launches": (c_i32, [ctypes.POINTER(AttnParams), ctypes.POINTER(c_i32)]),
+    "fdpp_ar_workspace_size": (c_i32, [c_i32, c_i64, ctypes.POINTER(c_sz)]),
+    "fdpp_ar_alloc": (c_i32, [c_sz, ctypes.POINTER(c_vp)]),
+    "fdpp_ar_free": (c_i32, [c_vp]),
+    "fdpp_ipc_get_handle": (c_i32, [c_vp, c_vp]),
+    "fdpp_ipc_open": (c_i32, [c_vp, ctypes.POINTER(c_vp)]),
+    "fdpp_ipc_close": (c_i32, [c_vp]),
+    "fdpp_ar_check": (c_i32, [c_vp, ctypes.POINTER(c_i32)]),
     "fdpp_attn_decode": (c_i32, [ctypes.POINTER(AttnParams), c_vp]),
     "fdpp_prepack_weight": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i64, c_i32, c_vp]),
     "fdpp_gemm_workspace_size": (c_i32, [c_i32, ctypes.POINTER(GemmParams), ctypes.POINTER(c_sz)]),

@@ -187,7 +187,21 @@ struct GemmFuse {
     int l2pf;                       // weight k-blocks prefetched to L2 ahead of the ring
     void *act_out;                  // epilogue: silu(gate) * up of tile-interleaved gate|up rows
     int64_t act_ld;
+    // epilogue: one-shot all-reduce over peer memory (row-parallel projections)
+    int ar_rank, ar_world;
+    int64_t ar_cap;                 // floats per (parity, source rank) receive slot
+    char *ar_ws[FDPP_AR_MAX_WORLD]; // every rank's all-reduce workspace, as mapped here
 };
+
+// All-reduce workspace (one per rank, peer-mapped): [0, 256) header (epoch,
+// CTA ticket, timeout error), then flags [world][kArSlices] (the epoch at
+// which source rank r published output slice s), then the receive buffers
+// [2 parities][world][ar_cap] fp32.  Epochs only grow, so a peer that is one
+// call ahead never hides this call's flag (waits test flag - epoch >= 0), and
+// its data lands in the other parity.
+constexpr int kArSlices = 8192;
+constexpr size_t kArHdr = 256;
+__host__ __device__ constexpr size_t ar_recv_off(int world) { return kArHdr + (size_t)world * kArSlices * 4; }
 
 // ImplA with the decode-step fusions (M <= 2, NR = 8 rows per CTA; the ImplB
 // fusions of fdpp_gemm_fuse in GEMV form): folded-RMSNorm row scale (x_op 3),
@@ -814,6 +828,7 @@ struct ClEpi {
     bool rope;
     const float *inv_rms;  // folded RMSNorm (nullptr: none)
     float *ssq;            // s_ssq[4][MMA_N] (nullptr: none)
+    float *stage;          // all-reduce: keep the rank-summed fp32 slice here instead of storing
 };
 
 template <typename T, int MMA_N>
@@ -840,8 +855,9 @@ template <typename T, int MMA_N, int CS>
 __device__ __forceinline__ void cl_reduce_store(const ClEpi<T> &e) {
     constexpr int PER = (((MMA_N + CS - 1) / CS) + 3) & ~3;  // this rank's columns
     // columns per round trip: every DSMEM load of a chunk in flight at once,
-    // <= 16 float4 of loads in registers
-    constexpr int NG = (PER / 4) < (16 / CS) ? (PER / 4) : (16 / CS);
+    // <= 16 float4 of loads and <= 32 residuals in registers
+    constexpr int NG_CAP = (16 / CS) < 8 ? (16 / CS) : 8;
+    constexpr int NG = (PER / 4) < NG_CAP ? (PER / 4) : NG_CAP;
     constexpr int CH = 4 * NG;
     const int n = e.n0 + e.row;
 #pragma unroll 1
@@ -876,7 +892,10 @@ __device__ __forceinline__ void cl_reduce_store(const ClEpi<T> &e) {
                 o[3] += buf[g][q].w;
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) cl_store_col<T, MMA_N>(e, cb + 4 * g + j, o[j], rv[4 * g + j]);
+            for (int j = 0; j < 4; ++j) {
+                if (e.stage) e.stage[(cb + 4 * g + j - e.c_beg) * 128 + e.row] = o[j];
+                else cl_store_col<T, MMA_N>(e, cb + 4 * g + j, o[j], rv[4 * g + j]);
+            }
         }
     }
 }
@@ -906,8 +925,79 @@ __device__ __forceinline__ void cl_reduce_store_any(const ClEpi<T> &e, int cs) {
         for (int j = 0; j < 4; ++j) {
             const int m = e.m0 + c + j;
             const float r = (e.R && m < e.M && n < e.N) ? Elem<T>::to_f(e.R[(int64_t)m * e.ldr + n]) : 0.f;
-            cl_store_col<T, MMA_N>(e, c + j, o[j], r);
+            if (e.stage) e.stage[(c + j - e.c_beg) * 128 + e.row] = o[j];
+            else cl_store_col<T, MMA_N>(e, c + j, o[j], r);
         }
+    }
+}
+
+__device__ __forceinline__ void st_release_sys_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// One-shot all-reduce of this CTA's output slice (columns [c_beg, c_end) x its
+// 128 weight rows), fused into the epilogue of a row-parallel projection: the
+// rank-summed fp32 slice (e.stage) is pushed into every peer's receive buffer
+// with plain stores over peer memory (NVLink), published by one release store
+// of the epoch per peer, the peers' slices are awaited (acquire), then C = the
+// sum over source ranks in rank order (+ residual, once) goes through the
+// normal store path (ssq_out included).  Every rank runs the same grid, so
+// slice ids match.  A wait that outlasts ~1 s sets the header's error word and
+// gives up (no hang; the host reports FDPP_ERR_CUDA-class failure).
+template <typename T, int MMA_N>
+__device__ __forceinline__ void cl_allreduce(const ClEpi<T> &e, const GemmFuse &fz, int slice, uint32_t epoch,
+                                             int tid) {
+    const int world = fz.ar_world, me = fz.ar_rank, par = (int)(epoch & 1u);
+    const int n = e.n0 + e.row;
+    auto recv = [&](int owner, int src) {
+        return reinterpret_cast<float *>(fz.ar_ws[owner] + ar_recv_off(world)) +
+               ((int64_t)par * world + src) * fz.ar_cap;
+    };
+    for (int c = e.c_beg; c < e.c_end; ++c) {
+        const int m = e.m0 + c;
+        if (m >= e.M || n >= e.N) continue;
+        const float v = e.stage[(c - e.c_beg) * 128 + e.row];
+        for (int r = 0; r < world; ++r)
+            if (r != me) recv(r, me)[(int64_t)m * e.N + n] = v;
+    }
+    __threadfence_system();
+    named_bar_sync(1, 128);
+    uint32_t *my_flags = reinterpret_cast<uint32_t *>(fz.ar_ws[me] + kArHdr);
+    if (tid == 0) {
+        for (int r = 0; r < world; ++r)
+            if (r != me)
+                st_release_sys_u32(reinterpret_cast<uint32_t *>(fz.ar_ws[r] + kArHdr) + (size_t)me * kArSlices + slice,
+                                   epoch);
+        for (int r = 0; r < world; ++r) {
+            if (r == me) continue;
+            const uint32_t *f = my_flags + (size_t)r * kArSlices + slice;
+            for (long it = 0; (int)(ld_acquire_sys_u32(f) - epoch) < 0; ++it) {
+                if (it > (1l << 22)) {  // ~1 s of 256 ns naps: report, never hang the GPU
+                    atomicExch(reinterpret_cast<unsigned int *>(fz.ar_ws[me]) + 2, 1u);
+                    break;
+                }
+                __nanosleep(256);
+            }
+        }
+    }
+    named_bar_sync(1, 128);
+    ClEpi<T> out = e;
+    out.stage = nullptr;
+    for (int c = e.c_beg; c < e.c_end; ++c) {
+        const int m = e.m0 + c;
+        const bool valid = m < e.M && n < e.N;
+        float tot = 0.f, rv = 0.f;
+        if (valid) {
+            for (int r = 0; r < world; ++r)  // rank order: the same sum on every rank
+                tot += r == me ? e.stage[(c - e.c_beg) * 128 + e.row] : __ldcg(recv(me, r) + (int64_t)m * e.N + n);
+            if (e.R) rv = Elem<T>::to_f(e.R[(int64_t)m * e.ldr + n]);
+        }
+        cl_store_col<T, MMA_N>(out, c, tot, rv);  // every lane: the ssq reduction is warp-wide
     }
 }
 
@@ -1028,14 +1118,23 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         const int per = (((MMA_N + ck.cs - 1) / ck.cs) + 3) & ~3;
         const int c_beg = (int)rank * per, c_end = min(MMA_N, c_beg + per);
         const bool rope = fz.q_out != nullptr, silu = fz.act_out != nullptr;
+        const bool ar = fz.ar_world > 1;
         ClEpi<T> ep{part, rbuf, C, ldc, R, ldr, M, N, n0, m0, c_beg, c_end, row, lane, quad, rope || silu,
-                    fz.x_op == 3 ? s_inv_rms : nullptr, fz.ssq_out ? &s_ssq[0][0] : nullptr};
+                    fz.x_op == 3 ? s_inv_rms : nullptr, fz.ssq_out ? &s_ssq[0][0] : nullptr,
+                    ar ? rbuf : nullptr};
+        if (ar) ep.R = nullptr;  // the residual is added once, after the exchange
         switch (ck.cs) {
             case 1: cl_reduce_store<T, MMA_N, 1>(ep); break;
             case 2: cl_reduce_store<T, MMA_N, 2>(ep); break;
             case 4: cl_reduce_store<T, MMA_N, 4>(ep); break;
             case 8: cl_reduce_store<T, MMA_N, 8>(ep); break;
             default: cl_reduce_store_any<T, MMA_N>(ep, ck.cs); break;
+        }
+        if (ar) {
+            ep.R = R;
+            const int slice = (tm * ck.n_tiles_n + tn) * ck.cs + (int)rank;
+            const uint32_t epoch = ld_volatile_u32(reinterpret_cast<const uint32_t *>(fz.ar_ws[fz.ar_rank])) + 1u;
+            cl_allreduce<T, MMA_N>(ep, fz, slice, epoch, threadIdx.x - 64);
         }
         if (fz.ssq_out || rope || silu) named_bar_sync(1, 128);
         if (silu && row < 64) {
@@ -1086,6 +1185,17 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         }
     }
     cluster_sync_all();  // peers may still be reading this CTA's partial
+    if (fz.ar_world > 1 && threadIdx.x == 64) {
+        // the last CTA to finish advances this rank's epoch for the next call
+        // (read by that kernel after its PDL wait, i.e. after this grid completes)
+        unsigned int *hdr = reinterpret_cast<unsigned int *>(fz.ar_ws[fz.ar_rank]);
+        __threadfence();
+        if (atomicAdd(hdr + 1, 1u) == gridDim.x * gridDim.y - 1) {
+            hdr[1] = 0u;
+            hdr[0] = hdr[0] + 1u;
+            __threadfence();
+        }
+    }
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, TMEM_COLS);
@@ -1377,7 +1487,7 @@ static int l2_prefetch_blocks() {
 // put the weight rows on the MMA M axis (swap-AB).
 static fdpp_status run_tc(const fdpp_gemm_params *p, bool flat, cudaStream_t st,
                           const fdpp_gemm_fuse *fuse = nullptr) {
-    const bool epi_fuse = fuse && (fuse->ssq_out || fuse->q_out || fuse->act_out);
+    const bool epi_fuse = fuse && (fuse->ssq_out || fuse->q_out || fuse->act_out || fuse->ar_world > 1);
     fdpp_status s = check_gemm(p, fuse && (fuse->q_out || fuse->act_out));
     if (s != FDPP_OK) return s;
     TcPlan pl;
@@ -1428,6 +1538,26 @@ static fdpp_status run_tc(const fdpp_gemm_params *p, bool flat, cudaStream_t st,
                      FDPP_ERR_VALUE, "SiLU epilogue needs N %% 128 == 0 (tile-interleaved gate|up)");
         L.fz.act_out = fuse->act_out;
         L.fz.act_ld = fuse->act_ld;
+        if (fuse->ar_world > 1) {
+            FDPP_REQUIRE(fuse->ar_world <= FDPP_AR_MAX_WORLD && fuse->ar_rank >= 0 &&
+                             fuse->ar_rank < fuse->ar_world,
+                         FDPP_ERR_VALUE, "all-reduce: rank %d of world %d (max %d)", fuse->ar_rank,
+                         fuse->ar_world, FDPP_AR_MAX_WORLD);
+            FDPP_REQUIRE(!fuse->q_out && !fuse->act_out && p->c != nullptr, FDPP_ERR_VALUE,
+                         "all-reduce epilogue writes C (no RoPE / SiLU epilogue)");
+            FDPP_REQUIRE(fuse->ar_cap >= (int64_t)p->M * p->N, FDPP_ERR_WORKSPACE,
+                         "all-reduce receive slot holds %lld floats, need M * N = %lld",
+                         (long long)fuse->ar_cap, (long long)p->M * p->N);
+            FDPP_REQUIRE((int64_t)pl.grid * pl.wk.n_tiles_m <= kArSlices, FDPP_ERR_SHAPE,
+                         "all-reduce: %d output slices exceed %d", pl.grid * pl.wk.n_tiles_m, kArSlices);
+            L.fz.ar_rank = fuse->ar_rank;
+            L.fz.ar_world = fuse->ar_world;
+            L.fz.ar_cap = fuse->ar_cap;
+            for (int r = 0; r < fuse->ar_world; ++r) {
+                FDPP_REQUIRE(fuse->ar_ws[r] != nullptr, FDPP_ERR_VALUE, "all-reduce workspace of rank %d is null", r);
+                L.fz.ar_ws[r] = static_cast<char *>(fuse->ar_ws[r]);
+            }
+        }
     }
     if ((s = make_kmajor_map(&L.mw, p->w, p->N, p->K, p->ldw, pl.bw, p->dtype)) != FDPP_OK) return s;
     if ((s = make_kmajor_map(&L.mx, p->a, p->M, p->K, p->lda, pl.bx, p->dtype)) != FDPP_OK) return s;
@@ -1623,6 +1753,64 @@ extern "C" fdpp_status fdpp_gemm_fused(const fdpp_gemm_params *p, const fdpp_gem
                                        void *stream) {
     FDPP_REQUIRE(fuse != nullptr, FDPP_ERR_VALUE, "null fuse descriptor");
     return run_tc(p, true, static_cast<cudaStream_t>(stream), fuse);
+}
+
+extern "C" fdpp_status fdpp_ar_workspace_size(int32_t world, int64_t cap, size_t *bytes) {
+    FDPP_REQUIRE(bytes != nullptr, FDPP_ERR_VALUE, "null output");
+    FDPP_REQUIRE(world >= 1 && world <= FDPP_AR_MAX_WORLD && cap >= 1, FDPP_ERR_VALUE,
+                 "all-reduce workspace: world %d (1..%d), cap %lld", world, FDPP_AR_MAX_WORLD, (long long)cap);
+    *bytes = ar_recv_off(world) + 2 * (size_t)world * (size_t)cap * sizeof(float);
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_ar_alloc(size_t bytes, void **ptr) {
+    FDPP_REQUIRE(ptr != nullptr && bytes > 0, FDPP_ERR_VALUE, "bad all-reduce allocation");
+    cudaError_t e = cudaMalloc(ptr, bytes);  // its own allocation: the IPC handle maps exactly it
+    if (e == cudaSuccess) e = cudaMemset(*ptr, 0, bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_status(e, "fdpp_ar_alloc");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_ar_free(void *ptr) {
+    cudaError_t e = cudaFree(ptr);
+    if (e != cudaSuccess) return cuda_status(e, "fdpp_ar_free");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_ipc_get_handle(void *ptr, void *handle64) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    FDPP_REQUIRE(ptr && handle64, FDPP_ERR_VALUE, "null pointer");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, ptr);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcGetMemHandle");
+    memcpy(handle64, &h, sizeof(h));
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_ipc_open(const void *handle64, void **ptr) {
+    FDPP_REQUIRE(ptr && handle64, FDPP_ERR_VALUE, "null pointer");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof(h));
+    cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcOpenMemHandle");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_ipc_close(void *ptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(ptr);
+    if (e != cudaSuccess) return cuda_status(e, "cudaIpcCloseMemHandle");
+    return FDPP_OK;
+}
+
+extern "C" fdpp_status fdpp_ar_check(const void *ws, int32_t *timed_out) {
+    FDPP_REQUIRE(ws && timed_out, FDPP_ERR_VALUE, "null pointer");
+    uint32_t hdr[4];
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(hdr, ws, sizeof(hdr), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_status(e, "fdpp_ar_check");
+    *timed_out = hdr[2] != 0u;
+    return FDPP_OK;
 }
 
 extern "C" fdpp_status fdpp_run_kernel(int32_t impl, const fdpp_gemm_params *p, void *stream) {

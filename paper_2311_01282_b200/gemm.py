@@ -210,7 +210,7 @@ def permute_gate_up_for_gemv(pw: PackedWeight) -> PackedWeight:
 
 def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ssq_in=None,
               ssq_tiles: int = 0, norm_w=None, eps: float = 1e-5, ssq_out=None, rope=None,
-              silu_out=None, impl: str = "B", stream=None, ws_tag="gemm"):
+              silu_out=None, impl: str = "B", stream=None, ws_tag="gemm", allreduce=None):
     """ImplB with the decode-step fusions (fdpp_gemm_fused).
 
     x_op 1: the activation tile is RMSNorm(a) * norm_w, with the rows' sums of
@@ -222,7 +222,10 @@ def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ss
     (QKV projection; ``out`` unused).  silu_out [M, N/2]: silu(gate) * up of a
     tile-interleaved gate|up weight (interleave_gate_up; ``out`` unused).
     impl "A": the GEMV form (fdpp_gemv_fused, M <= 2, x_op 0/3): ssq_out has
-    N/8 tiles, rope / silu_out need the permute_*_for_gemv weight layouts."""
+    N/8 tiles, rope / silu_out need the permute_*_for_gemv weight layouts.
+    allreduce (a ``PeerAllReduce``, row-parallel projections): C becomes the sum
+    of every rank's product plus ``residual`` once, exchanged inside the
+    epilogue over peer memory (no separate collective)."""
     torch = _torch()
     K = pw.ldw
     if x_op == 2:
@@ -260,6 +263,10 @@ def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ss
         fz.theta = float(rope.get("theta", 10000.0))
     if silu_out is not None:
         fz.act_out, fz.act_ld = silu_out.data_ptr(), silu_out.stride(0)
+    if allreduce is not None:
+        if impl == "A":
+            raise ValueError("the fused all-reduce runs in the ImplB cluster epilogue")
+        allreduce.fill(fz)
     lib = _lib.load()
     if impl == "A":
         _lib.check(lib.fdpp_gemv_fused(ctypes.byref(prm), ctypes.byref(fz), _lib.stream_handle(stream)),

@@ -103,13 +103,17 @@ class LlamaDecoder:
                  calib: ScalingCalibration = GOLDEN_CALIB, dtype=torch.float16, seed: int = 0,
                  attn_p: int = 0, attn_splits: int = 0, n_layers: int = None, fused: bool = True,
                  tp_rank: int = 0, tp_size: int = 1, group=None, weights: dict = None,
-                 collective: bool = True, gemv_step: bool = False):
+                 collective: bool = True, gemv_step: bool = False, allreduce=None):
         """tp_size > 1: this process is rank tp_rank of a tensor-parallel group
         (tp.py): sharded QKV / O / gate|up / down, local heads and KV cache, one
         NCCL all-reduce of the residual stream after O and after down (captured
         in the step's CUDA graph).  weights: optional FULL model weights
         {"layers": [{qkv, o, gate_up, down ([N, K]), ln1, ln2}], "embed",
-        "lm_head" ([vocab, hidden]), "ln_f"} to shard; default random init."""
+        "lm_head" ([vocab, hidden]), "ln_f"} to shard; default random init.
+        allreduce: a ``PeerAllReduce`` (allreduce.py) for this rank: the O / down
+        projections reduce across ranks inside their epilogue over peer memory
+        (residual and next-RMSNorm sums of squares fused too) instead of the
+        NCCL all-reduce + row-ssq kernel."""
         _lib.require_cuda()
         self.cfg, self.B, self.max_len, self.dtype = cfg, batch, max_len, dtype
         self.n_layers = n_layers or cfg.n_layers
@@ -117,6 +121,7 @@ class LlamaDecoder:
         # collective=False: one rank's shard alone on one GPU (per-GPU compute of a
         # t-way TP step; the all-reduce is omitted, the row-ssq kernel still runs)
         self.collective = collective
+        self.allreduce = allreduce if tp_size > 1 else None
         sd = _tp.shard_dims(cfg, tp_size)
         dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
@@ -205,6 +210,8 @@ class LlamaDecoder:
         # RoPE / SiLU stores; profiles/r1_bench).
         self.step_impl = ("A" if gemv_step and fused and B <= 2 and all(
             c == D.KernelChoice.IMPL_A for c in self.table_choices.values()) else "B")
+        if self.allreduce is not None:
+            self.step_impl = "B"  # the fused all-reduce lives in the ImplB cluster epilogue
         self.gemv_ssq_tiles = cfg.hidden // 8
         kind = D.KernelChoice.IMPL_A if self.step_impl == "A" else D.KernelChoice.IMPL_B
         self.choices = ({op: kind for op in shapes} if fused else dict(self.table_choices))
@@ -234,7 +241,7 @@ class LlamaDecoder:
         from .attention import launches
         na = launches(self.q, self.k_cache[0], self.attn_cfg, mode="async")
         if self.fused:
-            per_layer = 4 + na + (2 if self._tp_size > 1 else 0)
+            per_layer = 4 + na + (2 if self._tp_size > 1 and self.allreduce is None else 0)
             return 1 + self.n_layers * per_layer + 3
         return 1 + self.n_layers * (8 + na) + 4
 
@@ -321,8 +328,9 @@ class LlamaDecoder:
         lib = _lib.load()
         st = _lib.stream_handle()
         Hq, Dh = self.n_heads_local, cfg.head_dim
-        tp = self.tp_size > 1
-        lead = self.tp_rank == 0  # the rank whose row-parallel epilogue adds the residual
+        ar = self.allreduce        # fused peer-memory all-reduce in the O / down epilogues
+        tp = self.tp_size > 1 and ar is None  # separate NCCL all-reduce after O / down
+        lead = self.tp_rank == 0 or ar is not None  # ranks whose epilogue adds the residual
         impl = self.step_impl      # "B": tcgen05 flat GEMM; "A": fused GEMV (B <= 2)
         # sums-of-squares tiles the residual GEMMs leave for the next folded RMSNorm
         res_tiles = 1 if tp else (self.gemv_ssq_tiles if impl == "A" else self.ssq_tiles)
@@ -352,13 +360,15 @@ class LlamaDecoder:
                              seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed,
                              kv_prefetch=True)
             run_fused(self.attn.view(B, Hq * Dh), L["o"], out=self.x, residual=self.x if lead else None,
-                      ssq_out=None if tp or impl == "A" else self.ssq_b, ws_tag="decode_gemm", impl=impl)
+                      ssq_out=None if tp or impl == "A" else self.ssq_b, ws_tag="decode_gemm", impl=impl,
+                      allreduce=ar)
             if tp:
                 all_reduce_x(self.ssq_b)  # (the fused GEMV re-derives the norm from x itself)
             run_fused(self.x, L["gate_up_f"], x_op=3, ssq_in=self.ssq_b, silu_out=self.act,
                       ssq_tiles=res_tiles, eps=cfg.eps, ws_tag="decode_gemm", impl=impl)
             run_fused(self.act, L["down"], out=self.x, residual=self.x if lead else None,
-                      ssq_out=None if tp or impl == "A" else self.ssq_a, ws_tag="decode_gemm", impl=impl)
+                      ssq_out=None if tp or impl == "A" else self.ssq_a, ws_tag="decode_gemm", impl=impl,
+                      allreduce=ar)
             if tp:
                 all_reduce_x(self.ssq_a)
             ssq_tiles = res_tiles
