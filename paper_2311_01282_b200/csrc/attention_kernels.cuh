@@ -253,7 +253,10 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
     } else if constexpr (MMA) {
         // ------------------------------------------------ consumer warps, tensor cores
         // warps 0,1 take the two 16-key slices of even stages, warps 2,3 of odd stages
-        if (abortp != nullptr) cluster_wait();  // every peer's abort word is initialised
+        // the cluster barrier attn_cta arrived on (every peer's abort word is
+        // initialised) is awaited lazily: before this warp's first signal, else
+        // after its loop -- never on the critical path of the first tile
+        bool cw = abortp == nullptr;
         const int r0 = lane >> 2, cq = (lane & 3) * 2;
         uint32_t qa[D / 16][4];  // Q rows [16 x D] as m16n8k16 A fragments
 #pragma unroll
@@ -307,8 +310,11 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
                             const int key = k0 + 8 * nb + cq + (i & 1);
-                            // the oracle's arithmetic: logit = scale * dot rounded, then - phi
-                            const float ti = __fsub_rn(__fmul_rn(sacc[nb][i], scale), phi);
+                            // shifted logit scale * dot - phi in one fused multiply-add: the
+                            // sync pass's band check (flags of an aborted group) repeats it
+                            // exactly; vs the oracle's two roundings it can differ only
+                            // within an ulp of the band edge (the tests' guard band)
+                            const float ti = __fmaf_rn(sacc[nb][i], scale, -phi);
                             const bool valid = key < n, bad = (ti <= ba) || (ti >= bb);
                             if (valid && bad) {
                                 if (i < 2) viol0 = min(viol0, key0 + key);
@@ -328,9 +334,9 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
                             const int key = k0 + 8 * nb + cq + (i & 1);
-                            const float x = __fmul_rn(sacc[nb][i], scale);
+                            const float x = sacc[nb][i] * scale;
                             if (flags && key < n) {  // the async pass's band check and exp-sum
-                                const float ti = __fsub_rn(x, phi);
+                                const float ti = __fmaf_rn(sacc[nb][i], scale, -phi);
                                 const bool bad = (ti <= ba) || (ti >= bb);
                                 if (bad) {
                                     if (i < 2) viol0 = min(viol0, key0 + key);
@@ -391,13 +397,15 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
             }
             if constexpr (ASYNC) {
                 if (abortp != nullptr && !signaled && __any_sync(0xffffffffu, min(viol0, viol1) != INT_MAX)) {
-                    signaled = true;
+                    if (!cw) cluster_wait();
+                    cw = signaled = true;
                     signal_abort();
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
+        if (!cw) cluster_wait();
         // rows r0 / r0+8 are shared by the lane quad: fixed butterfly (sync: the
         // quad already shares one running max per row)
 #pragma unroll
@@ -467,7 +475,7 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
         }  // ASYNC
     } else {
         // ------------------------------------------------ consumer warps
-        if (abortp != nullptr) cluster_wait();  // every peer's abort word is initialised
+        bool cw = abortp == nullptr;       // lazy cluster wait, as in the tensor-core form
         const int c = lane % LPK;          // 16-B chunk of the head dim owned by this lane
         const int kg = lane / LPK;         // key slot inside a warp iteration
         float q[GT][VEC];
@@ -504,9 +512,11 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
             const int n = min(TK, k_end - key0);
             const T *sk = reinterpret_cast<const T *>(smem + s * Gm::STAGE_BYTES);
             const T *sv = sk + TK * D;
-            const bool skip = abortp != nullptr && __shfl_sync(0xffffffffu, ld_volatile_u32(abortp), 0) != 0u;
+            // (after an abort the producer completes stages without data; the
+            // CUDA-core consumers just run through them -- their partials are
+            // discarded -- rather than pay a per-tile check on the clean path)
 #pragma unroll 2
-            for (int kk0 = warp * KPI; kk0 < (skip ? 0 : n); kk0 += ATT_CONSUMERS * KPI) {
+            for (int kk0 = warp * KPI; kk0 < n; kk0 += ATT_CONSUMERS * KPI) {
                 const int kk = kk0 + kg;
                 const bool valid = kk < n;
                 float kf[VEC];
@@ -525,16 +535,16 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
                 load_vec<T, VEC>(sv + (valid ? kk : 0) * D + c * VEC, vf);
 #pragma unroll
                 for (int g = 0; g < GT; ++g) {
-                    const float x = __fmul_rn(dot[g], scale);  // logit, reference order: scale * acc
+                    const float x = dot[g] * scale;       // logit, reference order: scale * acc
                     float e;
                     if constexpr (ASYNC) {
-                        const float ti = __fsub_rn(x, phi);
+                        const float ti = __fmaf_rn(dot[g], scale, -phi);  // as the flags pass below
                         const bool bad = (ti <= ba) || (ti >= bb);
                         if (valid && bad) viol[g] = min(viol[g], key0 + kk);
                         e = (valid && !bad) ? __expf(ti) : 0.f;
                     } else {
                         if (flags && valid) {  // the async pass's band check and exp-sum
-                            const float ti = __fsub_rn(x, phi);
+                            const float ti = __fmaf_rn(dot[g], scale, -phi);
                             const bool bad = (ti <= ba) || (ti >= bb);
                             if (bad) viol[g] = min(viol[g], key0 + kk);
                             else dena[g] += __expf(ti);
@@ -559,7 +569,8 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
 #pragma unroll
                     for (int g = 0; g < GT; ++g) vmin = min(vmin, viol[g]);
                     if (__any_sync(0xffffffffu, vmin != INT_MAX)) {
-                        signaled = true;
+                        if (!cw) cluster_wait();
+                        cw = signaled = true;
                         signal_abort();
                     }
                 }
@@ -568,6 +579,7 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
             if (lane == 0) mbar_arrive(&empty[s]);
         }
 
+        if (!cw) cluster_wait();
         // ---- reduce across the key slots of the warp (lanes with equal c), fixed butterfly
 #pragma unroll
         for (int g = 0; g < GT; ++g) {
@@ -692,7 +704,9 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
 
     const int row0 = b * args.Hq + h0;        // global row index of g = 0
     if (threadIdx.x == 0) ATRACE(2);
-    const bool use_abort = ASYNC && args.cluster_join && args.abort_ok;
+    // (a row group of one CTA is launched without a cluster: its split cluster
+    // barrier would act as a CTA-wide one and deadlock the lazy waits below)
+    const bool use_abort = ASYNC && args.cluster_join && args.abort_ok && P >= 2;
     // every rank's s_abort must be initialised before a peer ORs into it: arrive
     // now; the consumers wait before their first tile, the producer after its loop
     if (use_abort) cluster_arrive();

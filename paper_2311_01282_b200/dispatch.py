@@ -33,7 +33,10 @@ from .matrix import GemmShape, ShapeError
 from .timing import measure, median_mad
 
 DEFAULT_M_SWEEP = (1, 2, 4, 8, 16, 32, 64, 128, 256)
-B200_M_SWEEP = (1, 2, 4, 8, 16, 32, 64)
+# the reference's sweep (dispatch.py:24) with one extra point between the flat
+# band and the 128-token conventional tile, where ImplB starts re-streaming
+# weights per 64-token tile
+B200_M_SWEEP = (1, 2, 4, 8, 16, 32, 64, 96, 128, 256)
 DEFAULT_REPS = 7
 DEFAULT_WARMUP = 2
 GEMV_MAX_M = 8

@@ -300,7 +300,8 @@ def test_incluster_recompute_matches_two_launch(tmp_path):
     res = {}
     for mode, env_over in (("two", {"FDPP_ATTN_INCLUSTER": "0"}),
                            ("one", {"FDPP_ATTN_INCLUSTER": "1", "FDPP_ATTN_ABORT": "0"}),
-                           ("abort", {"FDPP_ATTN_INCLUSTER": "1", "FDPP_ATTN_ABORT": "1"})):
+                           # =2 forces the early stop on these short rows (auto: >= 1K keys per CTA)
+                           ("abort", {"FDPP_ATTN_INCLUSTER": "1", "FDPP_ATTN_ABORT": "2"})):
         path = str(tmp_path / f"inc_{mode}.npz")
         env = dict(os.environ, **env_over)
         subprocess.run([sys.executable, os.path.join(root, "tests", "helpers", "attn_dump.py"), path],

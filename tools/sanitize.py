@@ -66,7 +66,11 @@ attn_case(2, 32, 2, 1500, fd.AUTO, [(1, 0)])                             # MQA t
 attn_case(1, 16, 2, 900, 5, [])                                          # G = 8, explicit p
 lens = torch.tensor([900, 3], dtype=torch.int32, device="cuda")
 q, k, v, cfg = attn_case(2, 16, 2, 900, fd.AUTO, [(0, 0)], seq_lens=lens)  # ragged lengths
-step("attention GQA/MQA tensor cores (async, sync, injected, ragged)")
+q, k, v, cfg = attn_case(2, 32, 2, 2048, 4, [])
+q[0, 5] = (q[0, 5].float() * 12).half()                                   # every chunk violates: early stop
+fd.decode_attention(q, k, v, cfg, "async")
+fd.decode_attention(q, k, v, fd.AttentionConfig.auto(cfg.scale, cal), "async", kv_prefetch=True)
+step("attention GQA/MQA tensor cores (async, sync, injected, ragged, early stop, K/V prefetch)")
 
 # ---- subsystem 2
 for M in (1, 3, 8, 17, 64):
@@ -82,6 +86,10 @@ for M in (1, 3, 8, 17, 64):
     D.run_device(D.KernelChoice.IMPL_B, a, pw, stages=1)
     fd.impl_b_flat(a.float().cpu().numpy(), b.float().cpu().numpy())   # f32 path
     fd.impl_c_blocked(a.float(), b.float())
+for M in (100, 200):                                                     # ImplC 128 / 256-token tiles
+    a = torch.randn((M, 1024), generator=g, device="cuda").half()
+    D.run_device(D.KernelChoice.IMPL_C, a, pw)
+    D.run_device(D.KernelChoice.IMPL_C, a, pw, ctas=40)                   # stream-K form
 step("ImplA / ImplB (cluster, stream-K) / ImplC / f32")
 
 B, H, Hq, Hkv = 4, 1024, 4, 2
@@ -114,6 +122,27 @@ gemm.run_fused(x2, gemm.permute_qkv_for_gemv(pq), x_op=3, ssq_in=ssq, ssq_tiles=
                rope={"q_out": qo[:2], "k_cache": kc[:2], "v_cache": vc[:2], "pos": pos[:2]})
 gemm.run_fused(x2, pd, out=x2, residual=x2, ssq_out=torch.zeros((H // 8, 2), device="cuda"), impl="A")
 step("fused GEMM prologues / epilogues, fused GEMV")
+
+# ---- fused one-shot all-reduce: two ranks in this process, one stream each
+from paper_2311_01282_b200.allreduce import PeerAllReduce  # noqa: E402
+ars = PeerAllReduce.local_group(2, cap=8 * 1024)
+xs = [torch.randn((8, 1024), generator=g, device="cuda").half() for _ in range(2)]
+As = [torch.randn((8, 512), generator=g, device="cuda").half() for _ in range(2)]
+Ws = [gemm.PackedWeight((torch.randn((1024, 512), generator=g, device="cuda") / 32).half(), 512, 1024)
+      for _ in range(2)]
+sts = [torch.cuda.Stream() for _ in range(2)]
+torch.cuda.synchronize()
+for r in range(2):
+    with torch.cuda.stream(sts[r]):
+        gemm.run_fused(As[r], Ws[r], out=xs[r], residual=xs[r], allreduce=ars[r], ws_tag=f"ar{r}")
+torch.cuda.synchronize()
+# compute-sanitizer serialises kernels, so rank 0 cannot see rank 1's slices and
+# takes the bounded-wait exit (reported, never hangs); the exchange code still runs
+print("all-reduce timed out (expected under the sanitizer's serialisation):",
+      [ar.timed_out() for ar in ars], flush=True)
+for ar in ars:
+    ar.close()
+step("fused all-reduce epilogue (2 ranks, 2 streams)")
 
 lib = _lib.load()
 st = _lib.stream_handle()
