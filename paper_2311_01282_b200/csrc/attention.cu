@@ -200,7 +200,7 @@ static fdpp_status layout_for(const fdpp_attn_params *p, AttnLayout *lay) {
 // CTAs and no per-chunk outputs are requested
 static bool cluster_join_for(const fdpp_attn_params *p, const AttnLayout &lay) {
     if (lay.P > 16 || lay.nsub != 1 || p->viol_index || p->chunk_num || p->chunk_den) return false;
-    return lay.mma || p->D <= ATT_THREADS;
+    return lay.mma || p->D <= ATT_CONSUMERS * 32;  // the producer warp reads the chunk states
 }
 
 // 2-D maps over the cache as [B * Hkv * Lmax rows, D]: 32-row x 64-column boxes

@@ -708,7 +708,8 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     // barrier would act as a CTA-wide one and deadlock the lazy waits below)
     const bool use_abort = ASYNC && args.cluster_join && args.abort_ok && P >= 2;
     // every rank's s_abort must be initialised before a peer ORs into it: arrive
-    // now; the consumers wait before their first tile, the producer after its loop
+    // now; the consumers wait before their first signal (or after their loop),
+    // the producer after its loop
     if (use_abort) cluster_arrive();
 
     attn_stream<T, D, GT, ASYNC, MMA>(args, tmK, tmV, smem, full, empty, red, false, 0, ntiles, k_begin, k_end,
@@ -724,9 +725,30 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
             // rows r, r + P, ...; chunk sums in chunk (= rank) order as the global join.
             __shared__ float s_dsum;
             uint32_t my_mask = 0u;  // rows this rank flagged (bit g)
-            cluster_sync_all();  // every rank's partial is in its shared memory (and every abort signal)
+            if constexpr (NRED > 1) {
+                // CUDA-core form: sum the consumer warps' partials into warp 0's buffer
+                // (warp order, as the join below always did) so peers read one value
+                // per element over DSMEM instead of NRED
+                for (int idx = threadIdx.x; idx < gcount * (D + 2); idx += ATT_THREADS) {
+                    const int g = idx / (D + 2), e = idx % (D + 2);
+                    if (e <= D) {
+                        float s = 0.f;
+#pragma unroll
+                        for (int w = 0; w < NRED; ++w) s += red[(w * GT + g) * (D + 2) + e];
+                        red[g * (D + 2) + e] = s;
+                    } else {
+                        int v = INT_MAX;
+#pragma unroll
+                        for (int w = 0; w < NRED; ++w) v = min(v, __float_as_int(red[(w * GT + g) * (D + 2) + e]));
+                        red[g * (D + 2) + e] = __int_as_float(v);
+                    }
+                }
+            }
+            if (threadIdx.x == 0) ATRACE(3);
             const uint32_t red_addr = smem_u32(red);
             const int rank = (int)cluster_ctarank();
+            cluster_sync_all();  // every rank's partial is in its shared memory (and every abort signal)
+            if (threadIdx.x == 0) ATRACE(4);
             // the group stopped streaming on a violation: its async partials are
             // incomplete, so every row is recomputed and flagged from the sync pass
             const bool aborted = use_abort && s_abort != 0u;
@@ -737,32 +759,33 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                     const uint32_t ra = red_addr + (uint32_t)(g * (D + 2)) * 4u;
                     int bad = 0;
                     float acc = 0.f;
-                    // a rank's chunk value = its NRED warp buffers summed in warp order
-                    constexpr uint32_t WSTRIDE = GT * (D + 2) * 4u;
+                    // every rank's value of this element requested at once (one DSMEM
+                    // round trip), then summed in chunk (= rank) order
                     for (int d = threadIdx.x; d < D; d += ATT_THREADS) {
-                        for (int q = 0; q < P; ++q) {  // chunk order
-                            float cv = 0.f;
+                        float cv[16];
 #pragma unroll
-                            for (int w = 0; w < NRED; ++w)
-                                cv += dsmem_ld_f32(dsmem_map_addr(ra + w * WSTRIDE + 4u * d, q));
-                            bad |= !isfinite(cv);
-                            acc += cv;
+                        for (int q = 0; q < 16; ++q)
+                            cv[q] = q < P ? dsmem_ld_f32_batched(dsmem_map_addr(ra + 4u * d, q)) : 0.f;
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            if (q < P) {
+                                bad |= !isfinite(cv[q]);
+                                acc += cv[q];
+                            }
                         }
                     }
-                    if (threadIdx.x == ATT_THREADS - 1) {
-                        float dsum = 0.f;
-                        for (int q = 0; q < P; ++q) {
-                            float dq = 0.f;
-                            int vq = INT_MAX;
-#pragma unroll
-                            for (int w = 0; w < NRED; ++w) {
-                                dq += dsmem_ld_f32(dsmem_map_addr(ra + w * WSTRIDE + 4u * D, q));
-                                vq = min(vq, __float_as_int(dsmem_ld_f32(dsmem_map_addr(ra + w * WSTRIDE + 4u * (D + 1), q))));
-                            }
-                            bad |= (vq != INT_MAX) || !isfinite(dq);  // non-finite chunk state = violation
-                            dsum += dq;
+                    if (warp == ATT_CONSUMERS) {  // the idle producer warp: lane q reads chunk q's state
+                        float dq = 0.f;
+                        int vq = INT_MAX;
+                        if (lane < P) {
+                            dq = dsmem_ld_f32_batched(dsmem_map_addr(ra + 4u * D, lane));
+                            vq = __float_as_int(dsmem_ld_f32_batched(dsmem_map_addr(ra + 4u * (D + 1), lane)));
                         }
-                        s_dsum = dsum;
+                        // a violating key or a non-finite chunk state is a violation
+                        bad |= __any_sync(0xffffffffu, lane < P && ((vq != INT_MAX) || !isfinite(dq)));
+                        float dsum = 0.f;
+                        for (int q = 0; q < P; ++q) dsum += __shfl_sync(0xffffffffu, dq, q);  // chunk order
+                        if (lane == 0) s_dsum = dsum;
                     }
                     const bool flagged = __syncthreads_or(bad) != 0;
                     if (threadIdx.x == 0) {
@@ -773,7 +796,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                         }
                     }
                     my_mask |= flagged ? (1u << g) : 0u;
-                    if (!flagged && threadIdx.x < D)  // D <= ATT_THREADS on this path (host check)
+                    if (!flagged && threadIdx.x < D)  // D <= 4 warps on this path (host check)
                         static_cast<T *>(args.o)[(int64_t)b * args.o_sb + (int64_t)(h0 + g) * args.o_sh + threadIdx.x] =
                             Elem<T>::from_f(acc / s_dsum);
                     __syncthreads();  // s_dsum is rewritten by the next row
@@ -783,6 +806,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
                 if (args.cluster_recompute && my_mask != 0u && threadIdx.x < P)
                     dsmem_red_or_u32(dsmem_map_addr(smem_u32(&s_gmask), threadIdx.x), my_mask);
                 cluster_sync_all();  // peers may still be reading this CTA's partial
+                if (threadIdx.x == 0) ATRACE(5);
                 gmask = s_gmask;     // the same on every rank
                 if (!args.cluster_recompute || gmask == 0u) return;
             } else {

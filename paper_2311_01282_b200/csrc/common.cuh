@@ -358,6 +358,13 @@ __device__ __forceinline__ float dsmem_ld_f32(uint32_t cluster_addr) {
     return v;
 }
 
+// 4-B DSMEM load with no memory clobber: loads of a loop issue back to back
+__device__ __forceinline__ float dsmem_ld_f32_batched(uint32_t cluster_addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(cluster_addr));
+    return v;
+}
+
 // 16-B DSMEM load with no memory clobber: a run of these issues back to back
 // (one round trip for all of them)
 __device__ __forceinline__ float4 dsmem_ld_v4(uint32_t cluster_addr) {

@@ -38,7 +38,7 @@ t = buf.astype(np.int64)
 ok = t[:, 0] > 0
 t = t[ok]
 base = t[:, 0].min()
-names = ["entry", "pdl_done", "setup", "published", "ticket", "joined", "consumers_done", "producer_done"]
+names = ["entry", "pdl_done", "setup", "published", "ticket/cluster_synced", "joined", "consumers_done", "producer_done"]
 print(f"B={B} Hq={Hq} Hkv={Hkv} L={L} plan={fd.attention.plan(q, k, cfg)} CTAs={len(t)}  (us from first entry)")
 for j, nm in enumerate(names):
     col = t[:, j]
