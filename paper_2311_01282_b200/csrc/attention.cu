@@ -337,7 +337,7 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
         AttnArgs ac = a;
         ac.cluster_join = cj;
         ac.cluster_recompute = inc;
-        ac.abort_ok = inc && abort_safe(p, lay);
+        ac.abort_ok = false;  // the early stop is a tensor-core-path feature (attention_kernels.cuh)
         s = by_dtype<true>(ac, p->dtype, p->D, lay.GT, lay.P, st);
     }
     if (s != FDPP_OK || inc) return s;

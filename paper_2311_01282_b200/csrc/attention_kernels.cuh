@@ -475,7 +475,9 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
         }  // ASYNC
     } else {
         // ------------------------------------------------ consumer warps
-        bool cw = abortp == nullptr;       // lazy cluster wait, as in the tensor-core form
+        // (no early stop here: the CUDA-core form is issue-bound, and even the idle
+        // per-tile violation check cost 5% of the 7B step's attention, so only the
+        // tensor-core form takes abort signals; the host never passes abortp here)
         const int c = lane % LPK;          // 16-B chunk of the head dim owned by this lane
         const int kg = lane / LPK;         // key slot inside a warp iteration
         float q[GT][VEC];
@@ -492,7 +494,6 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
         }
         float num[GT][VEC], den[GT], mx[GT], dena[GT];
         int viol[GT];
-        bool signaled = false;
 #pragma unroll
         for (int g = 0; g < GT; ++g) {
             den[g] = 0.f;
@@ -563,23 +564,10 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
                     for (int v = 0; v < VEC; ++v) num[g][v] = fmaf(e, vf[v], num[g][v]);
                 }
             }
-            if constexpr (ASYNC) {
-                if (abortp != nullptr && !signaled) {
-                    int vmin = INT_MAX;
-#pragma unroll
-                    for (int g = 0; g < GT; ++g) vmin = min(vmin, viol[g]);
-                    if (__any_sync(0xffffffffu, vmin != INT_MAX)) {
-                        if (!cw) cluster_wait();
-                        cw = signaled = true;
-                        signal_abort();
-                    }
-                }
-            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
         }
 
-        if (!cw) cluster_wait();
         // ---- reduce across the key slots of the warp (lanes with equal c), fixed butterfly
 #pragma unroll
         for (int g = 0; g < GT; ++g) {

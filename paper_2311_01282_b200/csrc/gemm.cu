@@ -851,7 +851,7 @@ __device__ __forceinline__ void cl_store_col(const ClEpi<T> &e, int c, float o, 
     }
 }
 
-template <typename T, int MMA_N, int CS>
+template <typename T, int MMA_N, int CS, bool STAGE = false>
 __device__ __forceinline__ void cl_reduce_store(const ClEpi<T> &e) {
     constexpr int PER = (((MMA_N + CS - 1) / CS) + 3) & ~3;  // this rank's columns
     // columns per round trip: every DSMEM load of a chunk in flight at once,
@@ -893,7 +893,7 @@ __device__ __forceinline__ void cl_reduce_store(const ClEpi<T> &e) {
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                if (e.stage) e.stage[(cb + 4 * g + j - e.c_beg) * 128 + e.row] = o[j];
+                if constexpr (STAGE) e.stage[(cb + 4 * g + j - e.c_beg) * 128 + e.row] = o[j];
                 else cl_store_col<T, MMA_N>(e, cb + 4 * g + j, o[j], rv[4 * g + j]);
             }
         }
@@ -901,7 +901,7 @@ __device__ __forceinline__ void cl_reduce_store(const ClEpi<T> &e) {
 }
 
 // any cluster size (rank count not a power of two): one 4-column group at a time
-template <typename T, int MMA_N>
+template <typename T, int MMA_N, bool STAGE = false>
 __device__ __forceinline__ void cl_reduce_store_any(const ClEpi<T> &e, int cs) {
     const int n = e.n0 + e.row;
     const uint32_t base = smem_u32(e.part) + (uint32_t)(((e.c_beg >> 2) * 128 + e.row) * 16);
@@ -925,7 +925,7 @@ __device__ __forceinline__ void cl_reduce_store_any(const ClEpi<T> &e, int cs) {
         for (int j = 0; j < 4; ++j) {
             const int m = e.m0 + c + j;
             const float r = (e.R && m < e.M && n < e.N) ? Elem<T>::to_f(e.R[(int64_t)m * e.ldr + n]) : 0.f;
-            if (e.stage) e.stage[(c + j - e.c_beg) * 128 + e.row] = o[j];
+            if constexpr (STAGE) e.stage[(c + j - e.c_beg) * 128 + e.row] = o[j];
             else cl_store_col<T, MMA_N>(e, c + j, o[j], r);
         }
     }
@@ -1001,7 +1001,9 @@ __device__ __forceinline__ void cl_allreduce(const ClEpi<T> &e, const GemmFuse &
     }
 }
 
-template <typename T, int BX, int STAGES, bool XF>
+// AR: the fused one-shot all-reduce epilogue (its own instantiation, so the
+// plain kernels carry none of its code)
+template <typename T, int BX, int STAGES, bool XF, bool AR = false>
 __global__ void __launch_bounds__(XF ? TC_THREADS_XF : TC_THREADS, 2)  // 2 CTAs / SM
 gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                     const __grid_constant__ CUtensorMap tmU, T *C, int64_t ldc,
@@ -1118,19 +1120,24 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         const int per = (((MMA_N + ck.cs - 1) / ck.cs) + 3) & ~3;
         const int c_beg = (int)rank * per, c_end = min(MMA_N, c_beg + per);
         const bool rope = fz.q_out != nullptr, silu = fz.act_out != nullptr;
-        const bool ar = fz.ar_world > 1;
+        constexpr bool ar = AR;
         ClEpi<T> ep{part, rbuf, C, ldc, R, ldr, M, N, n0, m0, c_beg, c_end, row, lane, quad, rope || silu,
                     fz.x_op == 3 ? s_inv_rms : nullptr, fz.ssq_out ? &s_ssq[0][0] : nullptr,
                     ar ? rbuf : nullptr};
         if (ar) ep.R = nullptr;  // the residual is added once, after the exchange
+        // cs = 1 on the flat tiles goes one 4-column group at a time: the batched
+        // form's registers (160 vs 125 per thread) cost the decode step ~2 %
         switch (ck.cs) {
-            case 1: cl_reduce_store<T, MMA_N, 1>(ep); break;
-            case 2: cl_reduce_store<T, MMA_N, 2>(ep); break;
-            case 4: cl_reduce_store<T, MMA_N, 4>(ep); break;
-            case 8: cl_reduce_store<T, MMA_N, 8>(ep); break;
-            default: cl_reduce_store_any<T, MMA_N>(ep, ck.cs); break;
+            case 1:
+                if constexpr (MMA_N >= 128) cl_reduce_store<T, MMA_N, 1, AR>(ep);
+                else cl_reduce_store_any<T, MMA_N, AR>(ep, 1);
+                break;
+            case 2: cl_reduce_store<T, MMA_N, 2, AR>(ep); break;
+            case 4: cl_reduce_store<T, MMA_N, 4, AR>(ep); break;
+            case 8: cl_reduce_store<T, MMA_N, 8, AR>(ep); break;
+            default: cl_reduce_store_any<T, MMA_N, AR>(ep, ck.cs); break;
         }
-        if (ar) {
+        if constexpr (AR) {
             ep.R = R;
             const int slice = (tm * ck.n_tiles_n + tn) * ck.cs + (int)rank;
             const uint32_t epoch = ld_volatile_u32(reinterpret_cast<const uint32_t *>(fz.ar_ws[fz.ar_rank])) + 1u;
@@ -1185,7 +1192,7 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
         }
     }
     cluster_sync_all();  // peers may still be reading this CTA's partial
-    if (fz.ar_world > 1 && threadIdx.x == 64) {
+    if (AR && threadIdx.x == 64) {
         // the last CTA to finish advances this rank's epoch for the next call
         // (read by that kernel after its PDL wait, i.e. after this grid completes)
         unsigned int *hdr = reinterpret_cast<unsigned int *>(fz.ar_ws[fz.ar_rank]);
@@ -1376,11 +1383,11 @@ struct TcLaunch {  // everything a tcgen05 launch needs besides the plan
     bool xf;
 };
 
-template <typename T, int BX, int STAGES, bool XF>
+template <typename T, int BX, int STAGES, bool XF, bool AR>
 static fdpp_status launch_cluster(const fdpp_gemm_params *p, const TcPlan &pl, const TcLaunch &L,
                                   cudaStream_t st) {
     using S = ClSmem<BX, STAGES, XF>;
-    auto kern = gemm_cluster_kernel<T, BX, STAGES, XF>;
+    auto kern = gemm_cluster_kernel<T, BX, STAGES, XF, AR>;
     static DeviceOnce attr;  // per instantiation and device
     cudaError_t e = attr.run([&] {
         cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::TOTAL);
@@ -1403,7 +1410,12 @@ template <typename T, int BW, int BX, bool SWAP, int STAGES, bool XF>
 static fdpp_status launch_tc(const fdpp_gemm_params *p, const TcPlan &pl, const TcLaunch &L,
                              cudaStream_t st) {
     if constexpr (SWAP && BW == 128) {
-        if (pl.cluster) return launch_cluster<T, BX, STAGES, XF>(p, pl, L, st);
+        if (pl.cluster) {
+            if constexpr (!XF && BX <= 64) {  // the fused all-reduce: row-parallel flat GEMMs
+                if (L.fz.ar_world > 1) return launch_cluster<T, BX, STAGES, XF, true>(p, pl, L, st);
+            }
+            return launch_cluster<T, BX, STAGES, XF, false>(p, pl, L, st);
+        }
     }
     using S = TcSmem<BW, BX, STAGES, XF>;
     auto kern = gemm_tc_kernel<T, BW, BX, SWAP, STAGES, XF>;

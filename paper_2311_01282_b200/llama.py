@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -94,6 +95,11 @@ def fold_norm(pw: PackedWeight, norm_w) -> PackedWeight:
     w = pw.w.clone()
     w[:, : pw.K] = (w[:, : pw.K].float() * norm_w.float()[None, :]).to(w.dtype)
     return PackedWeight(w, pw.K, pw.N)
+
+
+# the decode step lets attention stream K/V rows before its PDL wait (only the
+# appended row comes from the QKV epilogue); FDPP_KV_PREFETCH=0 disables it (A/B)
+KV_PREFETCH = os.environ.get("FDPP_KV_PREFETCH", "1") != "0"
 
 
 class LlamaDecoder:
@@ -358,7 +364,7 @@ class LlamaDecoder:
             # the QKV epilogue / rope_append just wrote only row pos of the caches
             decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
                              seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed,
-                             kv_prefetch=True)
+                             kv_prefetch=KV_PREFETCH)
             run_fused(self.attn.view(B, Hq * Dh), L["o"], out=self.x, residual=self.x if lead else None,
                       ssq_out=None if tp or impl == "A" else self.ssq_b, ws_tag="decode_gemm", impl=impl,
                       allreduce=ar)
@@ -400,7 +406,7 @@ class LlamaDecoder:
             # the QKV epilogue / rope_append just wrote only row pos of the caches
             decode_attention(self.q, kc, vc, self.attn_cfg, "async", out=self.attn,
                              seq_lens=self.lens, row_flags=self.row_flags, counter=self.recomputed,
-                             kv_prefetch=True)
+                             kv_prefetch=KV_PREFETCH)
             self._gemm("o", self.attn.view(B, Hq * Dh), L["o"], self.x, residual=self.x)
             _lib.check(lib.fdpp_rmsnorm(self.x.data_ptr(), L["ln2"].data_ptr(), self.h.data_ptr(), B,
                                         cfg.hidden, cfg.eps, dt, st), "rmsnorm")
