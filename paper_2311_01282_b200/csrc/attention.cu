@@ -89,6 +89,16 @@ static bool abort_safe(const fdpp_attn_params *p, const AttnLayout &lay) {
     return std::exp((double)p->b) * (double)p->L * 65504.0 < 1e37;
 }
 
+// FDPP_ATTN_EARLY_TRIGGER=0: one-wave launches trigger their dependents after
+// the main loop like multi-wave ones (A/B).
+static bool early_trigger_enabled() {
+    static int v = [] {
+        const char *e = getenv("FDPP_ATTN_EARLY_TRIGGER");
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 static bool mma_shape_ok(const fdpp_attn_params *p, int G) {
     if (!mma_enabled() || G < 4 || p->D != 128) return false;
     if (p->dtype != FDPP_F16 && p->dtype != FDPP_BF16) return false;
@@ -303,6 +313,7 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     a.cluster_recompute = false;
     a.abort_ok = false;
     a.kv_prefetch = p->kv_prefetch != 0;
+    a.early_trigger = false;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     a.kv_rows_per_head = p->kv_stride_h / p->D;
     const bool sync_mma = mma_shape_ok(p, lay.G);  // GQA/MQA sync softmax on tensor cores
@@ -324,8 +335,12 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     // one launch: the cluster recomputes its own flagged rows (sync softmax on the
     // same path the recompute launch would take)
     const bool inc = cj && incluster_enabled() && (lay.mma ? sync_mma : true);
+    // one wave: every CTA resident at once (3 per SM on both paths)
+    const int64_t ctas = (int64_t)lay.P * p->B * p->Hkv * (lay.mma ? lay.n_rg_mma : lay.n_rg);
+    const bool one_wave = ctas <= 3ll * (sm_count() > 0 ? sm_count() : 148) && early_trigger_enabled();
     if (lay.mma) {
         AttnArgs am = a;
+        am.early_trigger = one_wave && inc;
         am.n_rg = lay.n_rg_mma;
         am.cluster_join = cj;
         am.cluster_recompute = inc;
@@ -335,6 +350,7 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
         s = launch_mma<true>(am, p->dtype, lay.P, &mk, &mv, st);
     } else {
         AttnArgs ac = a;
+        ac.early_trigger = one_wave && inc;
         ac.cluster_join = cj;
         ac.cluster_recompute = inc;
         ac.abort_ok = false;  // the early stop is a tensor-core-path feature (attention_kernels.cuh)

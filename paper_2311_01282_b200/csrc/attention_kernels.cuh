@@ -67,6 +67,7 @@ struct AttnArgs {
     bool cluster_recompute;  // cluster_join: flagged rows are recomputed by the same cluster
     bool abort_ok;           // cluster_recompute: a violation stops the group's async stream
     bool kv_prefetch;        // async: stream K/V rows before the appended one ahead of the PDL wait
+    bool early_trigger;      // one-wave grid: let the next kernel launch at entry (PDL)
 };
 
 template <typename T, int D>
@@ -660,6 +661,10 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     // kv_prefetch the producer warp waits inside its loop instead (attn_stream)
     const int warp_id = threadIdx.x >> 5;
     if (!(ASYNC && args.kv_prefetch && warp_id == ATT_CONSUMERS)) pdl_wait();
+    // a grid that is resident in one wave has nothing to lose to its dependent's
+    // CTAs: let it launch now, so its prologue / weight or K/V prefetch overlaps
+    // this kernel instead of starting after its last CTA's main loop
+    if (ASYNC && args.early_trigger) pdl_trigger();
     if (threadIdx.x == 0) ATRACE(1);
     if (!ASYNC && args.only_flagged) {        // recompute launch: skip clean row groups
         int any = 0;

@@ -209,3 +209,42 @@ def test_gpu_entry_points_fail_loudly_without_cuda():
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         fd.batch_decode_attention(np.ones((1, 8), np.float32), np.ones((4, 8), np.float32),
                                   np.ones((4, 8), np.float32), cfg, "async")
+
+
+def _attn_prm(B, Hq, Hkv, L, p=0, spc=0, dtype=1, D=128):
+    from paper_2311_01282_b200 import _lib
+    prm = _lib.AttnParams()
+    prm.dtype, prm.B, prm.Hq, prm.Hkv, prm.L, prm.D = dtype, B, Hq, Hkv, L, D
+    prm.kv_stride_h, prm.kv_stride_b = L * D, Hkv * L * D
+    prm.scale, prm.phi, prm.a, prm.b = 0.088, -7.78, -1.0, 16.6
+    prm.p, prm.splits_per_chunk, prm.mode = p, spc, 0
+    return prm
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,L,p,spc,want", [
+    (1, 32, 32, 1024, 0, 0, 1),     # configs[0]: cluster join, recompute in the same launch
+    (32, 32, 32, 1024, 0, 0, 1),    # the 7B decode step
+    (8, 32, 2, 32768, 0, 0, 1),     # configs[3] MQA, tensor cores
+    (2, 32, 2, 2048, 7, 3, 2),      # sub-chunk splits: global join + recompute launch
+    (1, 4, 4, 600, 20, 0, 2),       # P > 16: no cluster
+])
+def test_attention_launch_count(B, Hq, Hkv, L, p, spc, want):
+    """fdpp_attn_launches (host-only): decode plans are one launch (the cluster
+    recomputes its own flagged rows); non-cluster plans keep the recompute launch."""
+    import ctypes
+    from paper_2311_01282_b200 import _lib
+    prm = _attn_prm(B, Hq, Hkv, L, p, spc)
+    n = ctypes.c_int32()
+    assert _lib.load().fdpp_attn_launches(ctypes.byref(prm), ctypes.byref(n)) == 0
+    assert n.value == want
+
+
+def test_allreduce_workspace_size():
+    """ar workspace = 256-B header + [world][8192] flags + 2 parities x world x cap floats."""
+    import ctypes
+    from paper_2311_01282_b200 import _lib
+    from paper_2311_01282_b200.allreduce import workspace_bytes
+    for world, cap in ((2, 4096), (8, 32 * 8192)):
+        assert workspace_bytes(world, cap) == 256 + world * 8192 * 4 + 2 * world * cap * 4
+    n = ctypes.c_size_t()
+    assert _lib.load().fdpp_ar_workspace_size(9, 16, ctypes.byref(n)) != 0   # world > FDPP_AR_MAX_WORLD
