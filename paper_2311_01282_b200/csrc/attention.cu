@@ -99,6 +99,15 @@ static bool early_trigger_enabled() {
     return v != 0;
 }
 
+// FDPP_ATTN_DEEP=0: every async launch keeps the 4-stage ring (A/B).
+static bool deep_ring_enabled() {
+    static int v = [] {
+        const char *e = getenv("FDPP_ATTN_DEEP");
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 static bool mma_shape_ok(const fdpp_attn_params *p, int G) {
     if (!mma_enabled() || G < 4 || p->D != 128) return false;
     if (p->dtype != FDPP_F16 && p->dtype != FDPP_BF16) return false;
@@ -314,6 +323,7 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     a.abort_ok = false;
     a.kv_prefetch = p->kv_prefetch != 0;
     a.early_trigger = false;
+    a.stages = ATT_STAGES;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     a.kv_rows_per_head = p->kv_stride_h / p->D;
     const bool sync_mma = mma_shape_ok(p, lay.G);  // GQA/MQA sync softmax on tensor cores
@@ -337,10 +347,16 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     const bool inc = cj && incluster_enabled() && (lay.mma ? sync_mma : true);
     // one wave: every CTA resident at once (3 per SM on both paths)
     const int64_t ctas = (int64_t)lay.P * p->B * p->Hkv * (lay.mma ? lay.n_rg_mma : lay.n_rg);
-    const bool one_wave = ctas <= 3ll * (sm_count() > 0 ? sm_count() : 148) && early_trigger_enabled();
+    const int nsm = sm_count() > 0 ? sm_count() : 148;
+    const bool one_wave = ctas <= 3ll * nsm && early_trigger_enabled();
+    // few CTAs per SM: give each a deeper K/V ring (more bytes in flight per SM);
+    // 6 x 16 KB keeps two CTAs per SM, 8 x 16 KB one
+    const int stages = !deep_ring_enabled() ? ATT_STAGES
+                       : ctas <= nsm ? ATT_MAX_STAGES : ctas <= 2ll * nsm ? 6 : ATT_STAGES;
     if (lay.mma) {
         AttnArgs am = a;
         am.early_trigger = one_wave && inc;
+        am.stages = stages;
         am.n_rg = lay.n_rg_mma;
         am.cluster_join = cj;
         am.cluster_recompute = inc;
@@ -351,6 +367,7 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     } else {
         AttnArgs ac = a;
         ac.early_trigger = one_wave && inc;
+        ac.stages = stages;
         ac.cluster_join = cj;
         ac.cluster_recompute = inc;
         ac.abort_ok = false;  // the early stop is a tensor-core-path feature (attention_kernels.cuh)
