@@ -89,25 +89,6 @@ static bool abort_safe(const fdpp_attn_params *p, const AttnLayout &lay) {
     return std::exp((double)p->b) * (double)p->L * 65504.0 < 1e37;
 }
 
-// FDPP_ATTN_EARLY_TRIGGER=0: one-wave launches trigger their dependents after
-// the main loop like multi-wave ones (A/B).
-static bool early_trigger_enabled() {
-    static int v = [] {
-        const char *e = getenv("FDPP_ATTN_EARLY_TRIGGER");
-        return e ? atoi(e) : 1;
-    }();
-    return v != 0;
-}
-
-// FDPP_ATTN_DEEP=0: every async launch keeps the 4-stage ring (A/B).
-static bool deep_ring_enabled() {
-    static int v = [] {
-        const char *e = getenv("FDPP_ATTN_DEEP");
-        return e ? atoi(e) : 1;
-    }();
-    return v != 0;
-}
-
 static bool mma_shape_ok(const fdpp_attn_params *p, int G) {
     if (!mma_enabled() || G < 4 || p->D != 128) return false;
     if (p->dtype != FDPP_F16 && p->dtype != FDPP_BF16) return false;
@@ -322,8 +303,7 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     a.cluster_recompute = false;
     a.abort_ok = false;
     a.kv_prefetch = p->kv_prefetch != 0;
-    a.early_trigger = false;
-    a.stages = ATT_STAGES;
+
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     a.kv_rows_per_head = p->kv_stride_h / p->D;
     const bool sync_mma = mma_shape_ok(p, lay.G);  // GQA/MQA sync softmax on tensor cores
@@ -345,18 +325,8 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     // one launch: the cluster recomputes its own flagged rows (sync softmax on the
     // same path the recompute launch would take)
     const bool inc = cj && incluster_enabled() && (lay.mma ? sync_mma : true);
-    // one wave: every CTA resident at once (3 per SM on both paths)
-    const int64_t ctas = (int64_t)lay.P * p->B * p->Hkv * (lay.mma ? lay.n_rg_mma : lay.n_rg);
-    const int nsm = sm_count() > 0 ? sm_count() : 148;
-    const bool one_wave = ctas <= 3ll * nsm && early_trigger_enabled();
-    // few CTAs per SM: give each a deeper K/V ring (more bytes in flight per SM);
-    // 6 x 16 KB keeps two CTAs per SM, 8 x 16 KB one
-    const int stages = !deep_ring_enabled() ? ATT_STAGES
-                       : ctas <= nsm ? ATT_MAX_STAGES : ctas <= 2ll * nsm ? 6 : ATT_STAGES;
     if (lay.mma) {
         AttnArgs am = a;
-        am.early_trigger = one_wave && inc;
-        am.stages = stages;
         am.n_rg = lay.n_rg_mma;
         am.cluster_join = cj;
         am.cluster_recompute = inc;
@@ -366,8 +336,6 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
         s = launch_mma<true>(am, p->dtype, lay.P, &mk, &mv, st);
     } else {
         AttnArgs ac = a;
-        ac.early_trigger = one_wave && inc;
-        ac.stages = stages;
         ac.cluster_join = cj;
         ac.cluster_recompute = inc;
         ac.abort_ok = false;  // the early stop is a tensor-core-path feature (attention_kernels.cuh)

@@ -33,8 +33,7 @@ namespace fdpp {
 
 constexpr int ATT_CONSUMERS = 4;                       // consumer warps
 constexpr int ATT_THREADS = (ATT_CONSUMERS + 1) * 32;  // + 1 producer warp
-constexpr int ATT_STAGES = 4;                          // ring depth of multi-wave grids
-constexpr int ATT_MAX_STAGES = 8;                      // one-wave grids with room for a deeper ring
+constexpr int ATT_STAGES = 4;
 constexpr int ATT_MAX_P = 1024;                        // semantic chunks per row
 
 struct AttnArgs {
@@ -68,8 +67,6 @@ struct AttnArgs {
     bool cluster_recompute;  // cluster_join: flagged rows are recomputed by the same cluster
     bool abort_ok;           // cluster_recompute: a violation stops the group's async stream
     bool kv_prefetch;        // async: stream K/V rows before the appended one ahead of the PDL wait
-    bool early_trigger;      // one-wave grid: let the next kernel launch at entry (PDL)
-    int stages;              // K/V ring depth (ATT_STAGES, or up to ATT_MAX_STAGES for <= 2 CTAs per SM)
 };
 
 template <typename T, int D>
@@ -203,7 +200,6 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
     const T *vbase = static_cast<const T *>(args.v) + (int64_t)b * args.kv_sb + (int64_t)kvh * args.kv_sh;
     (void)VEC; (void)LPK; (void)KPI; (void)kbase; (void)vbase;
     const bool flags = !ASYNC && wflags != nullptr;
-    const int nst = args.stages;  // ring depth (the host sizes shared memory for it)
     // signal an abort to every CTA of the cluster (once per warp)
     auto signal_abort = [&]() {
         if (lane == 0)
@@ -219,9 +215,9 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
         bool waited = !(ASYNC && args.kv_prefetch);
         if (lane == 0) {
             for (int t = 0; t < ntiles; ++t) {
-                const int s = (tbase + t) % nst;
-                const uint32_t ph = ((tbase + t) / nst) & 1;
-                if (!waited && (tbase + t >= nst || k_begin + (t + 1) * TK >= Lb)) {
+                const int s = (tbase + t) % ATT_STAGES;
+                const uint32_t ph = ((tbase + t) / ATT_STAGES) & 1;
+                if (!waited && (tbase + t >= ATT_STAGES || k_begin + (t + 1) * TK >= Lb)) {
                     pdl_wait();
                     waited = true;
                 }
@@ -285,8 +281,8 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
         const float scale = args.scale, phi = args.phi, ba = args.a, bb = args.b, ps = args.pscale;
         const int mi = lane >> 3, mr = lane & 7;  // ldmatrix: matrix / row this lane addresses
         for (int t = warp >> 1; t < ntiles; t += 2) {
-            const int s = (tbase + t) % nst;
-            mbar_wait(&full[s], ((tbase + t) / nst) & 1);
+            const int s = (tbase + t) % ATT_STAGES;
+            mbar_wait(&full[s], ((tbase + t) / ATT_STAGES) & 1);
             const int key0 = k_begin + t * TK;
             const int n = min(TK, k_end - key0);
             const uint32_t sk = smem_u32(smem + s * Gm::STAGE_BYTES), sv = sk + TK * RB;
@@ -510,8 +506,8 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
         const float scale = args.scale, phi = args.phi, ba = args.a, bb = args.b;
 
         for (int t = 0; t < ntiles; ++t) {
-            const int s = (tbase + t) % nst;
-            const uint32_t ph = ((tbase + t) / nst) & 1;
+            const int s = (tbase + t) % ATT_STAGES;
+            const uint32_t ph = ((tbase + t) / ATT_STAGES) & 1;
             mbar_wait(&full[s], ph);
             const int key0 = k_begin + t * TK;
             const int n = min(TK, k_end - key0);
@@ -638,9 +634,9 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     // (an integer offset from the shared array keeps the pointer in the shared
     // window, so every access below compiles to LDS/STS, not generic LD/ST)
     uint8_t *smem = MMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + args.stages * Gm::STAGE_BYTES);
-    uint64_t *empty = full + ATT_MAX_STAGES;
-    float *red = reinterpret_cast<float *>(empty + ATT_MAX_STAGES);  // [NRED][GT][D+2]
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + ATT_STAGES * Gm::STAGE_BYTES);
+    uint64_t *empty = full + ATT_STAGES;
+    float *red = reinterpret_cast<float *>(empty + ATT_STAGES);  // [NRED][GT][D+2]
     // join scratch aliases the K/V ring (free once every tile has been consumed)
     float *s_cden = reinterpret_cast<float *>(smem);
     int *s_cviol = reinterpret_cast<int *>(smem) + ATT_MAX_P;
@@ -664,10 +660,6 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     // kv_prefetch the producer warp waits inside its loop instead (attn_stream)
     const int warp_id = threadIdx.x >> 5;
     if (!(ASYNC && args.kv_prefetch && warp_id == ATT_CONSUMERS)) pdl_wait();
-    // a grid that is resident in one wave has nothing to lose to its dependent's
-    // CTAs: let it launch now, so its prologue / weight or K/V prefetch overlaps
-    // this kernel instead of starting after its last CTA's main loop
-    if (ASYNC && args.early_trigger) pdl_trigger();
     if (threadIdx.x == 0) ATRACE(1);
     if (!ASYNC && args.only_flagged) {        // recompute launch: skip clean row groups
         int any = 0;
@@ -690,7 +682,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     if (threadIdx.x == 0) {
         s_gmask = 0u;  // peers OR into it only after the first cluster barrier
         s_abort = 0u;  // peers OR into it only after the cluster launch's initial sync below
-        for (int s = 0; s < args.stages; ++s) {
+        for (int s = 0; s < ATT_STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], MMA ? 2 : ATT_CONSUMERS);  // MMA: two warps per stage
         }
@@ -1216,16 +1208,14 @@ template <typename T, int D, int GT, bool ASYNC, bool MMA = false>
 static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st,
                                const CUtensorMap *tmK = nullptr, const CUtensorMap *tmV = nullptr) {
     using Gm = AttnGeom<T, D>;
-    const int smem = (MMA ? 1024 : 0) + a.stages * Gm::STAGE_BYTES + 2 * ATT_MAX_STAGES * 8 +
+    const int smem = (MMA ? 1024 : 0) + ATT_STAGES * Gm::STAGE_BYTES + 2 * ATT_STAGES * 8 +
                      ((MMA && ASYNC) ? 1 : ATT_CONSUMERS) * GT * (D + 2) * (int)sizeof(float);
     auto kern = attn_split_kernel<T, D, GT, ASYNC, MMA>;
     CUtensorMap none;
     memset(&none, 0, sizeof(none));
     static DeviceOnce attr;  // per instantiation and device
     cudaError_t e0 = attr.run([&] {
-        // sized for the deepest ring any launch of this kernel may use
-        const int smem_max = smem + (ATT_MAX_STAGES - a.stages) * Gm::STAGE_BYTES;
-        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (r == cudaSuccess)  // cluster join: up to 16 CTAs per cluster
             r = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         return r;
