@@ -19,6 +19,7 @@ import paper_2311_01282_b200 as fd  # noqa: E402
 D = importlib.import_module("paper_2311_01282_b200.dispatch")
 peak, _ = bench._peaks()
 Ms = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [32, 64, 96, 128, 192, 256]
+only_m = os.environ.get("CONV_SWEEP_M")
 res = []
 for n, k in ((12288, 4096), (4096, 4096), (11008, 4096), (4096, 11008), (22016, 4096)):
     nrot = max(4, min(16, int(1.2e9 // (n * k * 2))))
@@ -28,7 +29,11 @@ for n, k in ((12288, 4096), (4096, 4096), (11008, 4096), (4096, 11008), (22016, 
         out = torch.empty((m, n), device="cuda", dtype=torch.half)
         byt = n * k * 2 + m * k * 2 + m * n * 2
         for name, ch, kw in (("B", D.KernelChoice.IMPL_B, {}), ("C", D.KernelChoice.IMPL_C, {}),
-                             ("C-streamK", D.KernelChoice.IMPL_C, {"ctas": 148})):
+                             ("C-streamK", D.KernelChoice.IMPL_C, {"ctas": 148}),
+                             ("C-bx128", D.KernelChoice.IMPL_C, {"block_x": 128}),
+                             ("C-bx128-cs2", D.KernelChoice.IMPL_C, {"block_x": 128, "ctas": -2})):
+            if name.startswith("C-bx128") and m <= 128:
+                continue
             t = bench._rotating_graph_time(torch, [lambda w=w: D.run_device(ch, a, w, out=out, **kw) for w in ws])
             r = {"n": n, "k": k, "m": m, "impl": name, "us": round(t * 1e6, 2),
                  "gbs": round(byt / t / 1e9, 1), "frac": round(byt / t / 1e9 / peak, 3)}
