@@ -320,8 +320,15 @@ def run_gpu(args):
         group = groups[rank // tp]
     B, L, K, W = args.batch, args.kv_len, args.steps, args.warmup
     table = _load_table(D, cfg, tp)
+    ar = None
+    if args.ar == "fused" and tp > 1 and not shard_only:
+        # the O / down projections reduce across the TP group inside their GEMM
+        # epilogue over IPC-mapped peer memory (allreduce.py) instead of NCCL
+        from paper_2311_01282_b200.allreduce import PeerAllReduce
+        ar = PeerAllReduce.create(group, cap=B * cfg.hidden)
     dec = llama.LlamaDecoder(cfg, B, L + max(K, W) + 16, table=table, seed=1000 + rank // tp,
-                             tp_rank=tp_rank, tp_size=tp, group=group, collective=not shard_only)
+                             tp_rank=tp_rank, tp_size=tp, group=group, collective=not shard_only,
+                             allreduce=ar)
     dec.prefill_random(L, seed=2000 + rank // tp)
     if args.inject:
         # configs[3]: force the synchronized-softmax recompute: one key far
@@ -480,6 +487,8 @@ def run_gpu(args):
                 "chatglm2-6b": "chatglm2-6b MQA decode step (configs[3])",
                 "llama2-70b": "llama2-70b GQA decode step (configs[4])"}[args.model]
     par = f"dp{dp}" + (f"xtp{tp}" if tp > 1 and not shard_only else "")
+    if tp > 1 and not shard_only:
+        par += " (all-reduce: " + ("fused into the O/down epilogues, peer memory" if ar is not None else "NCCL") + ")"
     if shard_only:
         par = f"one tp{tp} shard on 1 GPU (all-reduce omitted)"
     line = {
@@ -527,6 +536,8 @@ def run_gpu(args):
                                 "extrapolation_factor": cfg.n_layers}
     if world > 1:
         dist.barrier()
+        if ar is not None:
+            ar.close()
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -593,6 +604,8 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the configs[0]/[1] sub-benchmarks")
     ap.add_argument("--model", default="llama2-7b", choices=sorted(MODELS))
     ap.add_argument("--tp", type=int, default=1, help="tensor-parallel ranks per replica (torchrun)")
+    ap.add_argument("--ar", default="nccl", choices=("nccl", "fused"),
+                    help="TP all-reduce: NCCL after the O/down GEMMs, or fused into their epilogues")
     ap.add_argument("--tp-shard", type=int, default=1,
                     help="single GPU: run rank 0's shard of a T-way TP step (all-reduce omitted)")
     ap.add_argument("--calibrate", type=float, default=0.0,
