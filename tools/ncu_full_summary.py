@@ -11,6 +11,9 @@ KEYS = [
     "launch__shared_mem_per_block_dynamic", "launch__occupancy_limit_shared_mem",
     "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__waves_per_multiprocessor",
     "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
     "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second",
 ]
