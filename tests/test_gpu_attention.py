@@ -353,3 +353,41 @@ def test_incluster_recompute_vs_oracle(fd, torch, B, Hq, Hkv, L):
     assert st.rows_recomputed == int(redo.sum())
     assert any(redo[b, h * G:(h + 1) * G].any() for b, h in groups)
     assert fd.rel_error_rowwise(o.float().cpu().numpy().reshape(-1, 128), ref.reshape(-1, 128)) <= TOL
+
+
+def test_early_stop_ragged_lengths_vs_oracle(fd, torch):
+    """The tensor-core path's early stop (auto plan, >= 1K keys per CTA) with
+    ragged per-row lengths and out-of-band keys inside some rows' attended
+    range (and one past a row's length, which must not flag it): flag sets
+    bit-exact against the oracle's redo on each row's own prefix, outputs
+    within the fp16 bar."""
+    B, Hq, Hkv, L, D = 4, 32, 2, 16384, 128
+    G = Hq // Hkv
+    q, k, v = _qkv(torch, B, Hq, Hkv, L, D, 41, torch.float16)
+    lens = torch.tensor([16384, 9000, 12001, 15999], dtype=torch.int32, device="cuda")
+    k[0, 1, 5000].mul_(40.0)      # inside row 0's range
+    k[1, 0, 8999].mul_(40.0)      # the last attended key of row 1
+    k[2, 1, 12500].mul_(40.0)     # past row 2's length: must not flag
+    calib = fd.ScalingCalibration(*GOLD_CAL, coverage=1.0)
+    cfg = fd.AttentionConfig.auto(1 / math.sqrt(D), calib)
+    p, _ = fd.attention.plan(q, k, cfg)
+    o, st = fd.decode_attention(q, k, v, cfg, "async", seq_lens=lens)
+    qn = q.float().cpu().numpy()
+    flags = st.row_mask.cpu().numpy()
+    oc = O.Calib(*GOLD_CAL)
+    n_redo = 0
+    for b, n in enumerate(lens.tolist()):
+        kb = k[b, :, :n].float().cpu().numpy()
+        vb = v[b, :, :n].float().cpu().numpy()
+        for h in range(Hkv):
+            Qg = qn[b, h * G:(h + 1) * G]
+            ref, _, redo = O.batch_decode_attention(Qg, kb[h], vb[h], p, cfg.scale, oc, "async")
+            clear, _ = O.row_guard_ok(Qg, kb[h], cfg.scale, oc)
+            assert clear.all()
+            assert np.array_equal(flags[b, h * G:(h + 1) * G], redo), (b, h)
+            assert fd.rel_error_rowwise(o[b, h * G:(h + 1) * G].float().cpu().numpy(), ref) <= TOL, (b, h)
+            n_redo += int(redo.sum())
+    # the injected groups are flagged; row 2's key past its length is covered by the
+    # bit-exact comparison with the oracle on the row's own prefix
+    assert flags[0, G:2 * G].any() and flags[1, :G].any()
+    assert st.rows_recomputed == n_redo
