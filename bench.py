@@ -328,7 +328,7 @@ def run_gpu(args):
         ar = PeerAllReduce.create(group, cap=B * cfg.hidden)
     dec = llama.LlamaDecoder(cfg, B, L + max(K, W) + 16, table=table, seed=1000 + rank // tp,
                              tp_rank=tp_rank, tp_size=tp, group=group, collective=not shard_only,
-                             allreduce=ar)
+                             allreduce=ar, gemv_step=args.gemv_step)
     dec.prefill_random(L, seed=2000 + rank // tp)
     if args.inject:
         # configs[3]: force the synchronized-softmax recompute: one key far
@@ -608,6 +608,8 @@ def main():
                     help="TP all-reduce: NCCL after the O/down GEMMs, or fused into their epilogues")
     ap.add_argument("--tp-shard", type=int, default=1,
                     help="single GPU: run rank 0's shard of a T-way TP step (all-reduce omitted)")
+    ap.add_argument("--gemv-step", action="store_true",
+                    help="B <= 2: run the fused step on the CUDA-core GEMV (fdpp_gemv_fused) instead of ImplB")
     ap.add_argument("--calibrate", type=float, default=0.0,
                     help="calibrate phi/band on the model's logits at this coverage (default: SURVEY a1's golden calibration)")
     ap.add_argument("--inject", type=int, default=0,
