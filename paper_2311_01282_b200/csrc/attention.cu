@@ -303,7 +303,6 @@ extern "C" fdpp_status fdpp_attn_decode(const fdpp_attn_params *p, void *stream)
     a.cluster_recompute = false;
     a.abort_ok = false;
     a.kv_prefetch = p->kv_prefetch != 0;
-
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     a.kv_rows_per_head = p->kv_stride_h / p->D;
     const bool sync_mma = mma_shape_ok(p, lay.G);  // GQA/MQA sync softmax on tensor cores

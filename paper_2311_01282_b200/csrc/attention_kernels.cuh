@@ -33,7 +33,7 @@ namespace fdpp {
 
 constexpr int ATT_CONSUMERS = 4;                       // consumer warps
 constexpr int ATT_THREADS = (ATT_CONSUMERS + 1) * 32;  // + 1 producer warp
-constexpr int ATT_STAGES = 4;
+constexpr int ATT_STAGES = 4;                          // K/V ring depth (the kernels' NST)
 constexpr int ATT_MAX_P = 1024;                        // semantic chunks per row
 
 struct AttnArgs {
@@ -186,7 +186,7 @@ __device__ __forceinline__ void flag_group(const AttnArgs &a, int b, int kvh) {
 // `wflags` (sync pass of an aborted group): the consumers also evaluate the
 // async band check and exp-sums per row (first violating key, sum e^(x-phi) over
 // in-band keys) so the group's flags can be derived exactly without the async pass.
-template <typename T, int D, int GT, bool ASYNC, bool MMA>
+template <typename T, int D, int GT, bool ASYNC, bool MMA, int NST = ATT_STAGES>
 __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensorMap &tmK, const CUtensorMap &tmV,
                                             uint8_t *smem, uint64_t *full, uint64_t *empty, float *red,
                                             const bool red_in_ring, const int tbase, const int ntiles,
@@ -200,6 +200,7 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
     const T *vbase = static_cast<const T *>(args.v) + (int64_t)b * args.kv_sb + (int64_t)kvh * args.kv_sh;
     (void)VEC; (void)LPK; (void)KPI; (void)kbase; (void)vbase;
     const bool flags = !ASYNC && wflags != nullptr;
+    constexpr int nst = NST;  // compile-time ring depth: a runtime modulo costs the issue-bound loop ~4 %
     // signal an abort to every CTA of the cluster (once per warp)
     auto signal_abort = [&]() {
         if (lane == 0)
@@ -215,9 +216,9 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
         bool waited = !(ASYNC && args.kv_prefetch);
         if (lane == 0) {
             for (int t = 0; t < ntiles; ++t) {
-                const int s = (tbase + t) % ATT_STAGES;
-                const uint32_t ph = ((tbase + t) / ATT_STAGES) & 1;
-                if (!waited && (tbase + t >= ATT_STAGES || k_begin + (t + 1) * TK >= Lb)) {
+                const int s = (tbase + t) % nst;
+                const uint32_t ph = ((tbase + t) / nst) & 1;
+                if (!waited && (tbase + t >= nst || k_begin + (t + 1) * TK >= Lb)) {
                     pdl_wait();
                     waited = true;
                 }
@@ -281,8 +282,8 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
         const float scale = args.scale, phi = args.phi, ba = args.a, bb = args.b, ps = args.pscale;
         const int mi = lane >> 3, mr = lane & 7;  // ldmatrix: matrix / row this lane addresses
         for (int t = warp >> 1; t < ntiles; t += 2) {
-            const int s = (tbase + t) % ATT_STAGES;
-            mbar_wait(&full[s], ((tbase + t) / ATT_STAGES) & 1);
+            const int s = (tbase + t) % nst;
+            mbar_wait(&full[s], ((tbase + t) / nst) & 1);
             const int key0 = k_begin + t * TK;
             const int n = min(TK, k_end - key0);
             const uint32_t sk = smem_u32(smem + s * Gm::STAGE_BYTES), sv = sk + TK * RB;
@@ -506,8 +507,8 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
         const float scale = args.scale, phi = args.phi, ba = args.a, bb = args.b;
 
         for (int t = 0; t < ntiles; ++t) {
-            const int s = (tbase + t) % ATT_STAGES;
-            const uint32_t ph = ((tbase + t) / ATT_STAGES) & 1;
+            const int s = (tbase + t) % nst;
+            const uint32_t ph = ((tbase + t) / nst) & 1;
             mbar_wait(&full[s], ph);
             const int key0 = k_begin + t * TK;
             const int n = min(TK, k_end - key0);
@@ -620,7 +621,7 @@ __device__ __forceinline__ void attn_stream(const AttnArgs &args, const CUtensor
     }
 }
 
-template <typename T, int D, int GT, bool ASYNC, bool MMA>
+template <typename T, int D, int GT, bool ASYNC, bool MMA, int NST = ATT_STAGES>
 __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap &tmK, const CUtensorMap &tmV,
                                          const int cta, const int by, const int b) {
     using Gm = AttnGeom<T, D>;
@@ -634,9 +635,9 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     // (an integer offset from the shared array keeps the pointer in the shared
     // window, so every access below compiles to LDS/STS, not generic LD/ST)
     uint8_t *smem = MMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + ATT_STAGES * Gm::STAGE_BYTES);
-    uint64_t *empty = full + ATT_STAGES;
-    float *red = reinterpret_cast<float *>(empty + ATT_STAGES);  // [NRED][GT][D+2]
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * Gm::STAGE_BYTES);
+    uint64_t *empty = full + NST;
+    float *red = reinterpret_cast<float *>(empty + NST);  // [NRED][GT][D+2]
     // join scratch aliases the K/V ring (free once every tile has been consumed)
     float *s_cden = reinterpret_cast<float *>(smem);
     int *s_cviol = reinterpret_cast<int *>(smem) + ATT_MAX_P;
@@ -682,7 +683,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     if (threadIdx.x == 0) {
         s_gmask = 0u;  // peers OR into it only after the first cluster barrier
         s_abort = 0u;  // peers OR into it only after the cluster launch's initial sync below
-        for (int s = 0; s < ATT_STAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], MMA ? 2 : ATT_CONSUMERS);  // MMA: two warps per stage
         }
@@ -700,7 +701,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
     // the producer after its loop
     if (use_abort) cluster_arrive();
 
-    attn_stream<T, D, GT, ASYNC, MMA>(args, tmK, tmV, smem, full, empty, red, false, 0, ntiles, k_begin, k_end,
+    attn_stream<T, D, GT, ASYNC, MMA, NST>(args, tmK, tmV, smem, full, empty, red, false, 0, ntiles, k_begin, k_end,
                                       b, kvh, h0, gcount, use_abort ? &s_abort : nullptr, P, nullptr, Lb);
     __syncthreads();
 
@@ -815,7 +816,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
             float *mflags = wflags + ATT_CONSUMERS * GT * 2;
             static_assert(ATT_STAGES * Gm::STAGE_BYTES >= (ATT_CONSUMERS * GT * (D + 4) + GT * 2) * 4,
                           "ring holds warp partials and flags");
-            attn_stream<T, D, GT, false, MMA>(args, tmK, tmV, smem, full, empty, wred, true, ntiles, ntiles,
+            attn_stream<T, D, GT, false, MMA, NST>(args, tmK, tmV, smem, full, empty, wred, true, ntiles, ntiles,
                                               k_begin, k_end, b, kvh, h0, gcount, nullptr, P,
                                               aborted ? wflags : nullptr, Lb);
             __syncthreads();
@@ -1163,7 +1164,7 @@ __device__ __forceinline__ void attn_cta(const AttnArgs &args, const CUtensorMap
 // launch (list_mode) instead walks the (batch, kv-head) groups the async join
 // flagged, with a small fixed grid: a clean step costs one near-empty wave
 // instead of B x Hkv x n_rg x P early-exit CTAs.
-template <typename T, int D, int GT, bool ASYNC, bool MMA = false>
+template <typename T, int D, int GT, bool ASYNC, bool MMA = false, int NST = ATT_STAGES>
 __global__ void __launch_bounds__(ATT_THREADS, MMA ? 3 : 1)  // MMA: 3 CTAs / SM (192 KB of ring in flight)
 attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV) {
@@ -1184,7 +1185,7 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
                 const int rg = (int)(r % args.n_rg);
                 const int e = __ldcg(&args.flag_list[r / args.n_rg]);  // b * Hkv + kvh
                 const int b = e / args.Hkv, kvh = e % args.Hkv;
-                attn_cta<T, D, GT, ASYNC, MMA>(args, tmK, tmV, x, kvh * args.n_rg + rg, b);
+                attn_cta<T, D, GT, ASYNC, MMA, NST>(args, tmK, tmV, x, kvh * args.n_rg + rg, b);
                 __syncthreads();  // shared memory is reused by the next item
             }
             // the last CTA clears the list and its dedupe markers (graph replay)
@@ -1201,16 +1202,16 @@ attn_split_kernel(const AttnArgs args, const __grid_constant__ CUtensorMap tmK,
             return;
         }
     }
-    attn_cta<T, D, GT, ASYNC, MMA>(args, tmK, tmV, blockIdx.x, blockIdx.y, blockIdx.z);
+    attn_cta<T, D, GT, ASYNC, MMA, NST>(args, tmK, tmV, blockIdx.x, blockIdx.y, blockIdx.z);
 }
 
-template <typename T, int D, int GT, bool ASYNC, bool MMA = false>
+template <typename T, int D, int GT, bool ASYNC, bool MMA = false, int NST = ATT_STAGES>
 static fdpp_status launch_attn(const AttnArgs &a, int grid_x, cudaStream_t st,
                                const CUtensorMap *tmK = nullptr, const CUtensorMap *tmV = nullptr) {
     using Gm = AttnGeom<T, D>;
-    const int smem = (MMA ? 1024 : 0) + ATT_STAGES * Gm::STAGE_BYTES + 2 * ATT_STAGES * 8 +
+    const int smem = (MMA ? 1024 : 0) + NST * Gm::STAGE_BYTES + 2 * NST * 8 +
                      ((MMA && ASYNC) ? 1 : ATT_CONSUMERS) * GT * (D + 2) * (int)sizeof(float);
-    auto kern = attn_split_kernel<T, D, GT, ASYNC, MMA>;
+    auto kern = attn_split_kernel<T, D, GT, ASYNC, MMA, NST>;
     CUtensorMap none;
     memset(&none, 0, sizeof(none));
     static DeviceOnce attr;  // per instantiation and device
