@@ -294,7 +294,12 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         torch.cuda.set_device(local)
+        # NCCL's init lines (communicator size per rank) make the N-rank launch observable
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if rank == 0:
+            print(f"bench: {world} ranks over NCCL (one process per GPU)", file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(0)
     import paper_2311_01282_b200 as fd

@@ -125,3 +125,74 @@ def test_tp2_step_matches_unsharded():
         assert err <= 2e-2, f"rank {rank}: rel err {err}"
     # the replicated LM head + argmax agree across ranks
     assert np.array_equal(got[0][2], got[1][2])
+
+
+def _nccl_worker(rank, world, port, q):
+    import importlib
+
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        from paper_2311_01282_b200 import llama, tp
+        D = importlib.import_module("paper_2311_01282_b200.dispatch")
+        cfg, W = _setup()
+        dec = llama.LlamaDecoder(cfg, 4, 72, table=_table(D, cfg, world), weights=W, tp_rank=rank,
+                                 tp_size=world, group=dist.group.WORLD)
+        full_k, full_v, ids, pos = _state(torch, cfg)
+        for li in range(cfg.n_layers):
+            dec.k_cache[li].copy_(tp.shard_cache(full_k[li].to(f"cuda:{rank}"), cfg, rank, world))
+            dec.v_cache[li].copy_(tp.shard_cache(full_v[li].to(f"cuda:{rank}"), cfg, rank, world))
+        dec.ids.copy_(ids)
+        dec.pos.copy_(pos)
+        dec.lens.copy_(pos + 1)
+        dec.capture()          # NCCL all-reduces inside the step's CUDA graph
+        dec.step()
+        torch.cuda.synchronize()
+        q.put((rank, dec.x.float().cpu().numpy(), dec.ids.cpu().numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp2_nccl_step_matches_unsharded():
+    """Two GPUs, one rank each, NCCL all-reduces captured in the CUDA graph:
+    the tensor-parallel step equals the unsharded decoder's (skipped on a
+    single-GPU box)."""
+    import importlib
+
+    import numpy as np
+    import torch
+    import torch.multiprocessing as mp
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    from paper_2311_01282_b200 import llama
+    D = importlib.import_module("paper_2311_01282_b200.dispatch")
+    cfg, W = _setup()
+    ref = llama.LlamaDecoder(cfg, 4, 72, table=_table(D, cfg, 1), weights=W)
+    kc, vc, ids, pos = _state(torch, cfg)
+    for li in range(cfg.n_layers):
+        ref.k_cache[li].copy_(kc[li])
+        ref.v_cache[li].copy_(vc[li])
+    ref.ids.copy_(ids)
+    ref.pos.copy_(pos)
+    ref.lens.copy_(pos + 1)
+    ref.enqueue_step()
+    torch.cuda.synchronize()
+    x_ref = ref.x.float().cpu().numpy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    for rank, x, nxt in got:
+        err = float((np.abs(x - x_ref).max(1) / np.abs(x_ref).max(1)).max())
+        assert err <= 2e-2, f"rank {rank}: rel err {err}"
+    assert np.array_equal(got[0][2], got[1][2])
