@@ -1,3 +1,4 @@
+# A/B on one box: the previous build (a copy of its tree with its own .so in .ab_old/) vs this one
 show() {
   python -c "
 import json;d=json.loads(open('$2').read().split('\n')[0]);print('$1', d['value'],d['ms_per_step'],d['kernels']['attention_async(+recompute)']['us'])"
