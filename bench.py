@@ -297,6 +297,7 @@ def run_gpu(args):
         # NCCL's init lines (communicator size per rank) make the N-rank launch observable
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # stdout carries only the JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         if rank == 0:
             print(f"bench: {world} ranks over NCCL (one process per GPU)", file=sys.stderr, flush=True)
