@@ -2,6 +2,7 @@
 // integer decision logic of subsystem 3 (heuristic dispatch) — the parts of
 // dispatch.py / softmax.py that are pure control flow, restated natively so a
 // C/Go/Java caller gets the same decisions as the Python wrapper.
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -27,7 +28,11 @@ fdpp_status cuda_status(cudaError_t e, const char *what) {
     return FDPP_ERR_CUDA;
 }
 
-static std::atomic<int> g_pdl{1};
+// FDPP_PDL=0 starts with programmatic dependent launch off (A/B); fdpp_set_pdl changes it
+static std::atomic<int> g_pdl{[] {
+    const char *e = getenv("FDPP_PDL");
+    return e ? (atoi(e) != 0 ? 1 : 0) : 1;
+}()};
 bool pdl_enabled() { return g_pdl.load(std::memory_order_relaxed) != 0; }
 
 int sm_count() {
