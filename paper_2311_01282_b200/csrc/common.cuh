@@ -9,6 +9,8 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <utility>
 
@@ -93,6 +95,14 @@ inline cudaError_t launch_kernel_cluster(void (*kern)(KArgs...), dim3 grid, dim3
     }
     cfg.attrs = attr;
     cfg.numAttrs = n;
+    static const bool occ_probe = getenv("FDPP_OCC_PROBE") != nullptr;  // dev: cluster residency
+    if (occ_probe && cluster_x > 1) {
+        int nc = -1;
+        cudaError_t oe = cudaOccupancyMaxActiveClusters(&nc, kern, &cfg);
+        fprintf(stderr, "[occ] grid %ux%u block %u smem %zu cluster %d: clusters %u, max active %d (%s)\n",
+                grid.x, grid.y, block.x, smem, cluster_x, grid.x * grid.y / cluster_x, nc,
+                cudaGetErrorString(oe));
+    }
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

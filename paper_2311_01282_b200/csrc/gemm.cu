@@ -796,6 +796,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ 
 // QKV projection (a 128-row weight tile is exactly one head).
 struct TcCluster {
     int n_tiles_n, kb_total, kb_per, cs;
+    int krot;  // k-order rotation per weight tile (0: every tile walks its range from the start)
 };
 
 template <int BX, int STAGES, bool XF>
@@ -1034,8 +1035,9 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     const uint32_t rank = cluster_ctarank();
     const int tn = blockIdx.x / ck.cs, tm = blockIdx.y;
     const int n0 = tn * BW, m0 = tm * BX;
-    const int kb0 = (int)rank * ck.kb_per;
-    const int nkb = min(ck.kb_total, kb0 + ck.kb_per) - kb0;  // >= 1 (host guarantees)
+    // balanced split: rank r owns k-blocks [r*kb/cs, (r+1)*kb/cs), >= 1 each (cs <= kb)
+    const int kb0 = (int)(((int64_t)rank * ck.kb_total) / ck.cs);
+    const int nkb = (int)(((int64_t)(rank + 1) * ck.kb_total) / ck.cs) - kb0;
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmW);
@@ -1054,8 +1056,12 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    // staggered k order: tiles start their range at different k-blocks, so the
+    // CTAs do not all read the same activation block at the same time
+    const int kr = ck.krot ? (int)(((int64_t)tn * ck.krot) % nkb) : 0;
     auto coord = [&](int i, int &kb, int &nr, int &mr) {
-        kb = kb0 + i;
+        const int j = i + kr;
+        kb = kb0 + (j >= nkb ? j - nkb : j);
         nr = n0;
         mr = m0;
     };
@@ -1309,6 +1315,19 @@ static int pick_block_x(int M, bool flat) {
 // takes a whole SM; every other tile runs two per SM.
 static int ctas_per_sm(int bx) { return bx >= 256 ? 1 : 2; }
 
+// Cluster split-K tiles walk their k-range starting at block (tile * 7) mod
+// range: without it every one-CTA-per-tile launch (gate|up, LM head) has all
+// CTAs reading the same activation block and the same 128-B column of every
+// weight row at once (measured 4-5 % on those shapes, 0.6 % on the 7B step,
+// profiles/r2/gemm_krot_wtile.txt).  FDPP_KROT overrides (0 = off).
+static int k_rotation() {
+    static int v = [] {
+        const char *e = getenv("FDPP_KROT");
+        return e ? atoi(e) : 7;
+    }();
+    return v;
+}
+
 static fdpp_status plan_tc(const fdpp_gemm_params *p, bool flat, TcPlan *pl) {
     const int kb_total = ceil_div(p->K, TC_BK);
     pl->bx = p->block_x > 0 ? p->block_x : pick_block_x(p->M, flat);
@@ -1346,8 +1365,9 @@ static fdpp_status plan_tc(const fdpp_gemm_params *p, bool flat, TcPlan *pl) {
         TcCluster &c = pl->ck;
         c.n_tiles_n = w.n_tiles_n;
         c.kb_total = kb_total;
-        c.kb_per = (kb_total + cs - 1) / cs;
-        c.cs = (kb_total + c.kb_per - 1) / c.kb_per;  // no empty rank
+        c.kb_per = (kb_total + cs - 1) / cs;  // the largest rank's share
+        c.cs = cs;                            // balanced ranges, none empty (cs <= kb_total)
+        c.krot = k_rotation();
         pl->grid = w.n_tiles_n * c.cs;
         pl->stages = p->stages > 0 ? p->stages : 0;
         return FDPP_OK;
