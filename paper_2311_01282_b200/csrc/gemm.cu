@@ -1304,8 +1304,17 @@ struct TcPlan {
 // and loops over 64-token tiles beyond that; ImplC (the conventional GEMM)
 // takes all of M <= 256 in one 128- or 256-wide tile, so every weight byte
 // meets every token in one MMA chain (256-token tiles beyond).
-static int pick_block_x(int M, bool flat) {
-    if (!flat) return M <= 128 ? 128 : 256;
+static int pick_block_x(int M, int N, bool flat) {
+    // ImplC beyond 128 tokens: two 128-token tiles per weight tile while they fit
+    // one wave of 2 CTAs/SM (both read the weight tile at once, the second from
+    // L2), else the 256-token tile (one per SM): measured 5-10 % faster on
+    // [12288 | 11008 | 4096, 4096] at M = 192/256, 1-3 % slower on [22016, 4096]
+    // (profiles/r2/conv_sweep_bx128.txt)
+    if (!flat) {
+        if (M <= 128) return 128;
+        const int sms = sm_count() > 0 ? sm_count() : 148;
+        return (int64_t)ceil_div(N, 128) * ceil_div(M, 128) <= 2 * sms ? 128 : 256;
+    }
     if (M <= 16) return 16;
     if (M <= 32) return 32;
     return 64;
@@ -1330,7 +1339,7 @@ static int k_rotation() {
 
 static fdpp_status plan_tc(const fdpp_gemm_params *p, bool flat, TcPlan *pl) {
     const int kb_total = ceil_div(p->K, TC_BK);
-    pl->bx = p->block_x > 0 ? p->block_x : pick_block_x(p->M, flat);
+    pl->bx = p->block_x > 0 ? p->block_x : pick_block_x(p->M, p->N, flat);
     if (flat) {
         FDPP_REQUIRE(pl->bx == 16 || pl->bx == 32 || pl->bx == 64, FDPP_ERR_VALUE,
                      "ImplB block_x must be 16, 32 or 64");

@@ -17,6 +17,7 @@ cap implc_m128 gemm_cluster_kernel 0 gemm
 cap implc_m256 gemm_cluster_kernel 3 gemm
 cap implb_o_m32 gemm_cluster_kernel 6 gemm
 cap gemv_fused gemv_fused_kernel 0 gemv_fused
+cap implb_gu_m32 gemm_cluster_kernel 1 gemm_gu
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"attn_split|gemm_|gemv|embed|argmax|advance|row_ssq|rmsnorm|rope_append|silu_mul" -c 600 --csv \
     --log-file gpurun_out/ncu/launches_decode_step.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-extras > /dev/null 2>&1
 ls -la gpurun_out/ncu; du -sh gpurun_out

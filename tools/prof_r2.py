@@ -43,6 +43,14 @@ if what in ("all", "gemm"):
             for w in ws:
                 D.run_device(ch, a, w)
         del ws
+if what == "gemm_gu":
+    # ImplB M=32 on the fused gate|up shape [22016, 4096]: one CTA per tile (staggered k order)
+    n, k = 22016, 4096
+    ws = [fd.PackedWeight((torch.randn((n, k), generator=g, device="cuda") / k ** 0.5).half(), k, n)
+          for _ in range(3)]
+    a = torch.randn((32, k), generator=g, device="cuda").half()
+    for w in ws:
+        D.run_device(D.KernelChoice.IMPL_B, a, w)
 if what in ("all", "gemv_fused"):
     # the fused-GEMV QKV (folded RMSNorm + RoPE + KV append), Llama-2-7B shapes, M = 1
     H, Hq, Hkv = 4096, 32, 32
