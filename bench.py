@@ -285,6 +285,25 @@ def config2_gemm_sweep(torch, fd, D, table, peak):
     return res
 
 
+def dispatch_report(D, table):
+    """dispatch has no roofline -- its host cost (done once per M
+    bucket at graph capture) and the reference's self-consistency criterion
+    (test_acceptance.py:187-195) on the committed B200 profile."""
+    path = os.path.join(ROOT, "tables", "b200_decode.medians.json")
+    with open(path) as f:
+        details = json.load(f)
+    ref = D.load_table(os.path.join(ROOT, "tables", "b200_decode.tbl"))
+    worst, bad = D.dispatch_regret(ref, details)
+    reps = 20000
+    t0 = time.perf_counter()
+    for i in range(reps):
+        D.dispatch(1 + (i & 63), 12288, 4096, table)
+    host_ns = (time.perf_counter() - t0) / reps * 1e9
+    return {"host_ns_per_call": round(host_ns, 1), "profile_points": sum(len(r) for r in details.values()),
+            "max_dispatched_over_best": round(worst, 4), "points_over_1.10x": len(bad),
+            "table": "tables/b200_decode.tbl (tools/make_table.py, profile_shape flow to M = 256)"}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -534,7 +553,8 @@ def run_gpu(args):
     }
     if rank == 0 and world == 1 and default_run and not args.no_extras:
         line["configs"] = {"c1_attention_op_b1_l1024": config1_attention_op(torch, fd, peak),
-                           "c2_gemm_dispatch_sweep": config2_gemm_sweep(torch, fd, D, table, peak)}
+                           "c2_gemm_dispatch_sweep": config2_gemm_sweep(torch, fd, D, table, peak),
+                           "c2_dispatch": dispatch_report(D, table)}
     if rank == 0 and world == 1 and not args.no_cpu:
         t_step, desc, cores = cpu_reference_step(B, L, cfg)
         line["cpu_baseline"] = {"value": round(B / t_step, 4), "unit": UNIT, "cores": cores,

@@ -159,6 +159,24 @@ def dispatch(m: int, n: int, k: int, table: DispatchTable) -> KernelChoice:
     return _FROM_CODE[_lib.load().fdpp_dispatch_choose(int(m), int(e.m1), int(e.m2))]
 
 
+def dispatch_regret(table: DispatchTable, details: dict, tol: float = 1.10):
+    """The reference's dispatch self-consistency criterion (test_acceptance.py:
+    187-195): at every profiled point the dispatched kernel's median is within
+    ``tol`` x the best of the three.  ``details`` maps "NxK" (or (n, k)) to the
+    profile_shape rows.  Returns (worst ratio, [(n, k, m, picked, ratio) > tol])."""
+    worst, bad = 1.0, []
+    for key, rows in details.items():
+        n, k = (int(x) for x in key.split("x")) if isinstance(key, str) else key
+        for row in rows:
+            picked = dispatch(row["m"], n, k, table).value
+            best = min(row["ImplA"], row["ImplB"], row["ImplC"])
+            ratio = row[picked] / best
+            worst = max(worst, ratio)
+            if ratio > tol:
+                bad.append((n, k, row["m"], picked, round(ratio, 3)))
+    return worst, bad
+
+
 def default_fingerprint(workers: int = None) -> str:
     """B200 analogue of dispatch.py:200-203: device, SM count, lib ABI."""
     try:

@@ -210,7 +210,8 @@ def permute_gate_up_for_gemv(pw: PackedWeight) -> PackedWeight:
 
 def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ssq_in=None,
               ssq_tiles: int = 0, norm_w=None, eps: float = 1e-5, ssq_out=None, rope=None,
-              silu_out=None, impl: str = "B", stream=None, ws_tag="gemm", allreduce=None):
+              silu_out=None, impl: str = "B", stream=None, ws_tag="gemm", allreduce=None,
+              stages: int = 0):
     """ImplB with the decode-step fusions (fdpp_gemm_fused).
 
     x_op 1: the activation tile is RMSNorm(a) * norm_w, with the rows' sums of
@@ -245,6 +246,7 @@ def run_fused(a, pw: PackedWeight, *, out=None, residual=None, x_op: int = 0, ss
         prm.r, prm.ldr = residual.data_ptr(), residual.stride(0)
     prm.M, prm.N, prm.K = M, pw.N, K
     prm.dtype = _lib.dtype_code(a.dtype)
+    prm.stages = int(stages)
     fz = _lib.GemmFuse()
     fz.x_op = int(x_op)
     if x_op in (1, 3):
