@@ -12,7 +12,7 @@ import paper_2311_01282_b200 as fd  # noqa: E402
 from mode_sweep_lib import graph_time  # noqa: E402
 
 D = importlib.import_module("paper_2311_01282_b200.dispatch")
-tag = os.environ.get("FDPP_KROT", "0")
+tag = "krot=" + os.environ.get("FDPP_KROT", "7") + " l2pd=" + os.environ.get("FDPP_L2PD", "0")
 for n, k in ((12288, 4096), (4096, 4096), (22016, 4096), (4096, 11008), (32000, 4096)):
     L = max(4, min(24, int(2.4e9 // (n * k * 2))))
     ws = [fd.PackedWeight((torch.randn((n, k), device="cuda") / k ** 0.5).half(), k, n) for _ in range(L)]
@@ -23,5 +23,5 @@ for n, k in ((12288, 4096), (4096, 4096), (22016, 4096), (4096, 11008), (32000, 
         t = min(graph_time(lambda: [D.run_device(D.KernelChoice.IMPL_B, a, w, out=out) for w in ws]) / L
                 for _ in range(3))
         res.append(f"M{m}:{t:6.2f}")
-    print(f"krot={tag} [{n},{k}] " + " ".join(res), flush=True)
+    print(f"{tag} [{n},{k}] " + " ".join(res), flush=True)
     del ws
