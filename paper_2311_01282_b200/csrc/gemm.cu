@@ -1364,10 +1364,19 @@ static fdpp_status plan_tc(const fdpp_gemm_params *p, bool flat, TcPlan *pl) {
     const int slots = ctas_per_sm(pl->bx) * sms;
     pl->cluster = (p->ctas == 0 && tiles <= slots) || p->ctas < 0;
     if (pl->cluster) {
-        // the largest power-of-two split that keeps every CTA in one wave
-        // (the 7B shapes: 8 / 2 / 1 as measured; the 70B shards get 4-16)
+        // the largest split whose clusters are all co-resident: measured, at most
+        // ~256 cluster CTAs run at once with two per SM (260-288 fall into a second
+        // wave: [4608, 4096] cs = 8 13.7 us vs cs = 7 9.5 us; [12288, 4096] cs = 3
+        // 26 us vs cs = 2 18 us); beyond 8 ranks only when cs = 8 leaves most SMs
+        // idle and every rank keeps >= 8 k-blocks (the DSMEM reduction over 11-16
+        // ranks costs more than it hides); >= 2 k-blocks per rank.  Llama-2-7B:
+        // 8 / 2 / 1; ChatGLM2 QKV 7; 70B QKV shards 3 / 6 / 8 / 16
+        // (profiles/r2/gemm_cs_fine.txt)
+        const int cs_cap = tiles * 8 < sms ? 16 : 8;
         int cs = 1;
-        while (cs < 16 && tiles * cs * 2 <= slots && kb_total / (cs * 2) >= 2) cs *= 2;
+        while (cs < cs_cap && tiles * (cs + 1) <= 256 * ctas_per_sm(pl->bx) / 2 &&
+               kb_total / (cs + 1) >= (cs + 1 > 8 ? 8 : 2))
+            ++cs;
         if (p->ctas < 0) cs = -p->ctas;
         cs = cs < 1 ? 1 : (cs > 16 ? 16 : cs);  // > 8: non-portable cluster size
         if (cs > kb_total) cs = kb_total;
