@@ -578,9 +578,10 @@ def run_reference(args):
     cfg = getattr(llama, MODELS[args.model])
     B, L = args.batch, args.kv_len
     ref = CpuReference(B, L, cfg)
-    # one warm-up layer (page-in, thread pool) and the LM head, untimed; the
+    # W warm-up layers (page-in, thread pool) and the LM head, untimed; the
     # timed steps are K full decoder layers, each the unit described above
-    ref.layer()
+    for _ in range(max(1, args.warmup)):
+        ref.layer()
     ref.lm_head()
     times = [ref.layer() for _ in range(args.steps)]
     t_step = ref.step_seconds(times)
@@ -588,7 +589,7 @@ def run_reference(args):
     value = B / t_step
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": 1, "ms_per_step": round(timed / args.steps * 1e3, 2), "higher_is_better": True,
+        "warmup": max(1, args.warmup), "ms_per_step": round(timed / args.steps * 1e3, 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
         "config": {"workload": f"{args.model} decode step (configs[2])", "model": f"{cfg.name} geometry, random-init",
                    "global_batch": B, "batch_per_gpu": B, "kv_len": L,
