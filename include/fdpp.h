@@ -149,6 +149,11 @@ typedef struct fdpp_gemm_params {
 fdpp_status fdpp_prepack_weight(const void *b_kn, void *w_nk, int32_t K, int32_t N,
                                 int64_t ldw, int32_t dtype, void *stream);
 fdpp_status fdpp_gemm_workspace_size(int32_t impl, const fdpp_gemm_params *p, size_t *bytes);
+/* Host-only plan query for ImplB / ImplC (no launch, no device work): CTAs in
+ * the grid, cluster split-K size (1 = no cluster; 0 = persistent stream-K) and
+ * the token tile on the MMA N axis -- what fdpp_run_kernel would launch. */
+fdpp_status fdpp_gemm_plan(int32_t impl, const fdpp_gemm_params *p, int32_t *ctas, int32_t *cluster,
+                           int32_t *block_x);
 
 /* ImplA (dispatch.py:73-90): CUDA-core GEMV for M <= 8, weights streamed
  * once for all rows (the reference re-streams B per row). */

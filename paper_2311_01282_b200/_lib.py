@@ -84,6 +84,8 @@ SIGNATURES = {
     "fdpp_attn_decode": (c_i32, [ctypes.POINTER(AttnParams), c_vp]),
     "fdpp_prepack_weight": (c_i32, [c_vp, c_vp, c_i32, c_i32, c_i64, c_i32, c_vp]),
     "fdpp_gemm_workspace_size": (c_i32, [c_i32, ctypes.POINTER(GemmParams), ctypes.POINTER(c_sz)]),
+    "fdpp_gemm_plan": (c_i32, [c_i32, ctypes.POINTER(GemmParams), ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
+                               ctypes.POINTER(c_i32)]),
     "fdpp_impl_a_gemv": (c_i32, [ctypes.POINTER(GemmParams), c_vp]),
     "fdpp_impl_b_flat": (c_i32, [ctypes.POINTER(GemmParams), c_vp]),
     "fdpp_impl_c_gemm": (c_i32, [ctypes.POINTER(GemmParams), c_vp]),

@@ -1716,6 +1716,19 @@ extern "C" fdpp_status fdpp_gemm_workspace_size(int32_t impl, const fdpp_gemm_pa
     return FDPP_OK;
 }
 
+extern "C" fdpp_status fdpp_gemm_plan(int32_t impl, const fdpp_gemm_params *p, int32_t *ctas,
+                                      int32_t *cluster, int32_t *block_x) {
+    FDPP_REQUIRE(p && ctas && cluster && block_x, FDPP_ERR_VALUE, "null pointer");
+    FDPP_REQUIRE(impl == FDPP_IMPL_B || impl == FDPP_IMPL_C, FDPP_ERR_VALUE, "plan query is for ImplB / ImplC");
+    TcPlan pl;
+    fdpp_status s = plan_tc(p, impl == FDPP_IMPL_B, &pl);
+    if (s != FDPP_OK) return s;
+    *ctas = pl.cluster ? pl.grid * pl.wk.n_tiles_m : pl.grid;  // stream-K: a 1-D persistent grid
+    *cluster = pl.cluster ? pl.ck.cs : 0;
+    *block_x = pl.bx;
+    return FDPP_OK;
+}
+
 extern "C" fdpp_status fdpp_impl_a_gemv(const fdpp_gemm_params *p, void *stream) {
     if (p && p->dtype == FDPP_F32) return run_gemm_f32(FDPP_IMPL_A, p, static_cast<cudaStream_t>(stream));
     fdpp_status s = check_gemm(p);

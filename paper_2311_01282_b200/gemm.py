@@ -146,6 +146,22 @@ def run(impl: int, a, pw: PackedWeight, *, out=None, residual=None, block_x=0, c
     return out
 
 
+def plan(impl: int, M: int, N: int, K: int, *, block_x: int = 0, ctas: int = 0):
+    """Host-only launch plan of ImplB (impl 1) / ImplC (impl 2) for an [M, K] x
+    [N, K] problem (fdpp_gemm_plan): (CTAs, cluster split-K size or 0 for the
+    persistent stream-K grid, token tile).  No device work."""
+    prm = _lib.GemmParams()
+    ld = (K + 7) // 8 * 8
+    prm.lda, prm.ldw, prm.ldc = ld, ld, N
+    prm.M, prm.N, prm.K = M, N, ld
+    prm.dtype = _lib.F16
+    prm.block_x, prm.ctas = block_x, ctas
+    c, cl, bx = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(_lib.load().fdpp_gemm_plan(impl, ctypes.byref(prm), ctypes.byref(c), ctypes.byref(cl),
+                                          ctypes.byref(bx)), "gemm_plan")
+    return c.value, cl.value, bx.value
+
+
 def reference_dtype(a):
     """Device dtype of a reference-signature call: fp16/bf16 tensors keep their
     dtype (tensor-core path); numpy arrays and float32 tensors compute in f32."""

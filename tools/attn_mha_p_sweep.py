@@ -14,7 +14,7 @@ import paper_2311_01282_b200 as fd  # noqa: E402
 
 peak, _ = bench._peaks()
 cal = fd.ScalingCalibration(phi=-7.775933742523193, a=-1.0, b=16.577659606933594, coverage=1.0)
-for B, L in ((4, 1024), (8, 1024), (16, 1024), (32, 1024), (8, 4096), (16, 4096)):
+for B, L in ((1, 1024), (2, 1024), (4, 1024), (1, 4096)) if len(sys.argv) > 1 else ((4, 1024), (8, 1024), (16, 1024), (32, 1024), (8, 4096), (16, 4096)):
     g = torch.Generator(device="cuda").manual_seed(0)
     q = torch.randn((B, 32, 128), generator=g, device="cuda").half()
     out = torch.empty_like(q)
@@ -24,7 +24,7 @@ for B, L in ((4, 1024), (8, 1024), (16, 1024), (32, 1024), (8, 4096), (16, 4096)
             torch.randn((B, 32, L, 128), generator=g, device="cuda").half()) for _ in range(nrot)]
     byt = kvbytes + 2 * B * 32 * 128 * 2
     row = {"B": B, "L": L}
-    for p in ["auto"] + list(range(1, 9)):
+    for p in ["auto"] + list(range(1, 17)):
         cfg = (fd.AttentionConfig.auto(1 / math.sqrt(128), cal) if p == "auto"
                else fd.AttentionConfig(p=p, scale=1 / math.sqrt(128), calib=cal, splits_per_chunk=1))
         fns = [lambda k=k, v=v: fd.decode_attention(q, k, v, cfg, "async", out=out, kv_prefetch=True) for k, v in kvs]
