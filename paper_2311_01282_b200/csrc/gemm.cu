@@ -1374,7 +1374,8 @@ static fdpp_status plan_tc(const fdpp_gemm_params *p, bool flat, TcPlan *pl) {
         // (profiles/r2/gemm_cs_fine.txt)
         const int cs_cap = tiles * 8 < sms ? 16 : 8;
         int cs = 1;
-        while (cs < cs_cap && tiles * (cs + 1) <= 256 * ctas_per_sm(pl->bx) / 2 &&
+        const int co_resident = 256 * sms / 148 * ctas_per_sm(pl->bx) / 2;  // measured on 148 SMs
+        while (cs < cs_cap && tiles * (cs + 1) <= co_resident &&
                kb_total / (cs + 1) >= (cs + 1 > 8 ? 8 : 2))
             ++cs;
         if (p->ctas < 0) cs = -p->ctas;
