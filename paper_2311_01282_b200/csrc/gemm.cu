@@ -1536,6 +1536,204 @@ static int l2_prefetch_blocks() {
 
 // flat = ImplB (16/32/64-token tiles), else ImplC (128/256-token tiles); both
 // put the weight rows on the MMA M axis (swap-AB).
+// ============================================================ ImplC, CTA pair (cta_group::2)
+// Conventional GEMM for M > 128 on a pair of SMs: one tcgen05.mma.cta_group::2
+// computes a 256-weight-row x BXP-token tile; each CTA of the pair stages 128
+// weight rows and BXP/2 tokens per k-block (its TMA loads complete on the
+// leader's barrier), so per output element each SM ingests half the token
+// bytes of the one-CTA 128-token tile.  The leader's elected thread issues the
+// MMAs and multicasts their commits to both CTAs; each CTA's TMEM holds its
+// 128 rows x BXP columns of the fp32 accumulator.
+__device__ __forceinline__ void tma_load_2d_pair(void *dst_smem, const CUtensorMap *map, uint64_t *bar,
+                                                 int32_t c0, int32_t c1, uint64_t policy) {
+    // both CTAs load; the transaction bytes land on the leader's (rank 0) barrier
+    const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst_smem)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(mbar), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {  // arrives on both CTAs' barrier
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+template <int BXP, int PER_SM>
+struct PairSmem {  // PER_SM CTAs per SM: a ~192 KB ring, or ~96 KB so two pairs share an SM pair
+    static constexpr uint32_t W_BYTES = 128 * TC_BK * 2;
+    static constexpr uint32_t X_BYTES = (BXP / 2) * TC_BK * 2;
+    static constexpr uint32_t STAGE_BYTES = W_BYTES + X_BYTES;
+    static constexpr int STAGES = (192 * 1024 / PER_SM) / STAGE_BYTES;
+    static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr uint32_t TOTAL = BAR_OFF + (2 * STAGES + 2) * 8 + 16 + 1024;
+};
+
+template <typename T, int BXP, int PER_SM>
+__global__ void __launch_bounds__(TC_THREADS, PER_SM)
+gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, T *C,
+                 int64_t ldc, const T *R, int64_t ldr, int M, int N, int K) {
+    using S = PairSmem<BXP, PER_SM>;
+    constexpr int STAGES = S::STAGES;
+    constexpr uint32_t IDESC = umma_idesc_f16(256, BXP, std::is_same<T, __nv_bfloat16>::value);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::BAR_OFF);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tmem_full = empty + STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int pair = blockIdx.x >> 1;
+    const int n0 = pair * 256 + (int)rank * 128;      // this CTA's weight rows
+    const int m0 = blockIdx.y * BXP;                   // the pair's tokens
+    const int nkb = (K + TC_BK - 1) / TC_BK;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmW);
+        prefetch_tmap(&tmX);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"((uint32_t)BXP)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            pdl_wait();
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
+                if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
+                uint8_t *st = smem + s * S::STAGE_BYTES;
+                tma_load_2d_pair(st, &tmW, &full[s], i * TC_BK, n0, kEvictFirst);
+                tma_load_2d_pair(st + S::W_BYTES, &tmX, &full[s], i * TC_BK, m0 + (int)rank * (BXP / 2), kEvictLast);
+            }
+            pdl_trigger();
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (rank == 0 && lane == 0) {
+            for (int i = 0; i < nkb; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&full[s], (i / STAGES) & 1);
+                tc_fence_after();
+                uint8_t *st = smem + s * S::STAGE_BYTES;
+                const uint64_t da = umma_desc_sw128(st);
+                const uint64_t db = umma_desc_sw128(st + S::W_BYTES);
+#pragma unroll
+                for (int k = 0; k < TC_BK / 16; ++k)
+                    umma_f16_pair(tmem_base, da + 2 * k, db + 2 * k, IDESC, (i == 0 && k == 0) ? 0u : 1u);
+                umma_commit_pair(&empty[s]);
+            }
+            umma_commit_pair(tmem_full);
+        }
+        __syncwarp();
+    } else {  // epilogue warps 2-5: TMEM lanes = this CTA's 128 weight rows
+        const int quad = warp & 3;
+        const int row = quad * 32 + lane;
+        const int n = n0 + row;
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        pdl_wait();
+#pragma unroll 1
+        for (int c0 = 0; c0 < BXP; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + c0, v);
+            if (n < N) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int m = m0 + c0 + j;
+                    if (m < M) {
+                        float o = v[j];
+                        if (R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
+                        C[(int64_t)m * ldc + n] = Elem<T>::from_f(o);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // the leader's MMAs read both CTAs' smem; TMEM reads done
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)BXP)
+                     : "memory");
+    }
+}
+
+template <typename T, int BXP, int PER_SM>
+static fdpp_status launch_pair(const fdpp_gemm_params *p, cudaStream_t st) {
+    using S = PairSmem<BXP, PER_SM>;
+    auto kern = gemm_pair_kernel<T, BXP, PER_SM>;
+    static DeviceOnce attr;
+    cudaError_t e = attr.run([&] {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::TOTAL);
+        if (r == cudaSuccess)
+            r = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
+        return r;
+    });
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(gemm_pair)");
+    CUtensorMap mw, mx;
+    fdpp_status s;
+    if ((s = make_kmajor_map(&mw, p->w, p->N, p->K, p->ldw, 128, p->dtype)) != FDPP_OK) return s;
+    if ((s = make_kmajor_map(&mx, p->a, p->M, p->K, p->lda, BXP / 2, p->dtype)) != FDPP_OK) return s;
+    const dim3 grid(2 * ceil_div(p->N, 256), ceil_div(p->M, BXP));
+    e = launch_kernel_cluster(kern, grid, dim3(TC_THREADS), S::TOTAL, st, 2, mw, mx, static_cast<T *>(p->c),
+                              p->ldc, static_cast<const T *>(p->r), p->ldr, p->M, p->N, p->K);
+    if (e != cudaSuccess) return cuda_status(e, "gemm_pair_kernel launch");
+    return FDPP_OK;
+}
+
+static int implc_pair_mode() {  // FDPP_IMPLC_PAIR: -1 auto (default), 0 off, 1 always (A/B)
+    static const int v = [] {
+        const char *e = getenv("FDPP_IMPLC_PAIR");
+        return e ? atoi(e) : -1;
+    }();
+    return v;
+}
+
+// ImplC beyond 128 tokens takes the CTA-pair kernel when its 256-row pairs
+// occupy at least half the SMs (fewer pairs leave most of the GPU idle: the
+// one-CTA plan splits K instead); ring sized for two pairs per SM pair when
+// the pairs outnumber the SM pairs.  Returns 0 (not used), 1 or 2 (CTAs / SM).
+static int implc_pair_plan(const fdpp_gemm_params *p) {
+    const int mode = implc_pair_mode();
+    if (mode == 0 || p->M <= 128 || p->M > 256 || p->block_x != 0 || p->ctas != 0) return 0;
+    const int sms = sm_count() > 0 ? sm_count() : 148;
+    const int pairs = ceil_div(p->N, 256);
+    if (mode < 0 && 4 * pairs < sms) return 0;
+    return 2 * pairs > sms ? 2 : 1;
+}
+
 static fdpp_status run_tc(const fdpp_gemm_params *p, bool flat, cudaStream_t st,
                           const fdpp_gemm_fuse *fuse = nullptr) {
     const bool epi_fuse = fuse && (fuse->ssq_out || fuse->q_out || fuse->act_out || fuse->ar_world > 1);
@@ -1721,6 +1919,12 @@ extern "C" fdpp_status fdpp_gemm_plan(int32_t impl, const fdpp_gemm_params *p, i
                                       int32_t *cluster, int32_t *block_x) {
     FDPP_REQUIRE(p && ctas && cluster && block_x, FDPP_ERR_VALUE, "null pointer");
     FDPP_REQUIRE(impl == FDPP_IMPL_B || impl == FDPP_IMPL_C, FDPP_ERR_VALUE, "plan query is for ImplB / ImplC");
+    if (impl == FDPP_IMPL_C && implc_pair_plan(p)) {  // the CTA-pair kernel
+        *ctas = 2 * ceil_div(p->N, 256) * ceil_div(p->M, 256);
+        *cluster = 2;
+        *block_x = 256;
+        return FDPP_OK;
+    }
     TcPlan pl;
     fdpp_status s = plan_tc(p, impl == FDPP_IMPL_B, &pl);
     if (s != FDPP_OK) return s;
@@ -1749,6 +1953,14 @@ extern "C" fdpp_status fdpp_impl_b_flat(const fdpp_gemm_params *p, void *stream)
 
 extern "C" fdpp_status fdpp_impl_c_gemm(const fdpp_gemm_params *p, void *stream) {
     if (p && p->dtype == FDPP_F32) return run_gemm_f32(FDPP_IMPL_C, p, static_cast<cudaStream_t>(stream));
+    if (const int per_sm = p ? implc_pair_plan(p) : 0) {
+        fdpp_status s = check_gemm(p);
+        if (s != FDPP_OK) return s;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        if (per_sm == 2)
+            return p->dtype == FDPP_BF16 ? launch_pair<__nv_bfloat16, 256, 2>(p, st) : launch_pair<__half, 256, 2>(p, st);
+        return p->dtype == FDPP_BF16 ? launch_pair<__nv_bfloat16, 256, 1>(p, st) : launch_pair<__half, 256, 1>(p, st);
+    }
     return run_tc(p, false, static_cast<cudaStream_t>(stream));
 }
 

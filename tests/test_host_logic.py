@@ -290,9 +290,13 @@ def test_gemm_plan_cluster_split(M, N, K, want):
 
 
 def test_gemm_plan_conventional_tiles():
-    """ImplC: 128-token tiles to M = 128; beyond, two 128-token tiles per weight
-    tile while they fit a wave, else the 256-token tile (conv_sweep_bx128.txt)."""
+    """ImplC: 128-token tiles to M = 128; beyond, the CTA-pair kernel (256 weight
+    rows x 256 tokens per cta_group::2 MMA) when its pairs cover half the SMs,
+    else two 128-token tiles per weight tile while they fit a wave, else the
+    256-token tile (profiles/r2/implc_pair.txt, conv_sweep_bx128.txt)."""
     from paper_2311_01282_b200 import gemm
     assert gemm.plan(2, 128, 12288, 4096)[2] == 128
-    assert gemm.plan(2, 256, 12288, 4096)[2] == 128   # 192 tiles of 128 tokens
-    assert gemm.plan(2, 256, 22016, 4096)[2] == 256   # 344 would not fit
+    assert gemm.plan(2, 256, 12288, 4096) == (96, 2, 256)    # 48 pairs
+    assert gemm.plan(2, 192, 22016, 4096) == (172, 2, 256)   # 86 pairs, two per SM pair
+    assert gemm.plan(2, 256, 4096, 4096) == (256, 4, 128)     # 16 pairs: one-CTA tiles, split-K
+    assert gemm.plan(2, 256, 8192, 8192)[2] == 128           # 32 pairs < half the SMs
