@@ -168,7 +168,9 @@ fdpp_status fdpp_impl_b_flat(const fdpp_gemm_params *p, void *stream);
  * M <= 256 tokens in one 128- or 256-wide tile (weights on the MMA M axis),
  * so each weight byte is multiplied by every token in one MMA chain rather
  * than once per 64-token flat tile; cluster split-K while its tiles fit one
- * wave, persistent stream-K beyond. */
+ * wave, persistent stream-K beyond.  129-256 tokens with N >= ~9.5K run on
+ * 2-CTA clusters: one tcgen05.mma.cta_group::2 per 256 weight rows x 256
+ * tokens, each CTA staging half the tokens. */
 fdpp_status fdpp_impl_c_gemm(const fdpp_gemm_params *p, void *stream);
 /* run_kernel(choice, a, b) (dispatch.py:155-156). */
 fdpp_status fdpp_run_kernel(int32_t impl, const fdpp_gemm_params *p, void *stream);

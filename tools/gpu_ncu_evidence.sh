@@ -14,8 +14,8 @@ cap attn_mha attn_split_kernel 0 attn
 cap attn_mqa attn_split_kernel 2 attn
 cap gemv gemv_kernel 0 gemm
 cap implc_m128 gemm_cluster_kernel 0 gemm
-cap implc_m256 gemm_cluster_kernel 3 gemm
-cap implb_o_m32 gemm_cluster_kernel 6 gemm
+cap implc_m256 gemm_pair_kernel 0 gemm
+cap implb_o_m32 gemm_cluster_kernel 3 gemm
 cap gemv_fused gemv_fused_kernel 0 gemv_fused
 cap implb_gu_m32 gemm_cluster_kernel 1 gemm_gu
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"attn_split|gemm_|gemv|embed|argmax|advance|row_ssq|rmsnorm|rope_append|silu_mul" -c 600 --csv \
