@@ -111,6 +111,27 @@ def test_conventional_regime(fd, torch, N, K, M):
     assert max(errs.values()) <= TOL, errs
 
 
+@pytest.mark.parametrize("N,K,M,dt", [(12288, 4096, 256, "float16"), (1408 + 11 * 1024, 1024, 129, "float16"),
+                                      (22016, 4096, 192, "float16"), (12288, 4096, 200, "bfloat16")])
+def test_conventional_cta_pair(fd, torch, N, K, M, dt):
+    """ImplC beyond 128 tokens on 2-CTA clusters (tcgen05.mma.cta_group::2):
+    against the oracle, with a residual, a partial last pair (N % 256 != 0),
+    the two-pairs-per-SM-pair ring ([22016, 4096]) and bf16; the plan query
+    confirms the pair path is the one that ran; bitwise reruns."""
+    from paper_2311_01282_b200 import gemm
+    D = __import__("importlib").import_module("paper_2311_01282_b200.dispatch")
+    dtype = getattr(torch, dt)
+    a, b = _operands(torch, M, N, K, 3 * M + N, dtype)
+    pw = fd.pack_weight(b)
+    assert gemm.plan(2, M, N, K)[1:] == (2, 256)
+    r = (torch.randn((M, N), device="cuda") * 0.1).to(dtype)
+    out = D.run_device(D.KernelChoice.IMPL_C, a, pw, residual=r)
+    ref = _oracle(a, b) + r.float().cpu().numpy()
+    tol = TOL if dt == "float16" else 8e-3
+    assert fd.rel_error_rowwise(out.float().cpu().numpy(), ref) <= tol
+    assert torch.equal(out, D.run_device(D.KernelChoice.IMPL_C, a, pw, residual=r))
+
+
 def test_bf16(fd, torch):
     a, b = _operands(torch, 16, 4096, 4096, 5, torch.bfloat16)
     ref = _oracle(a, b)
