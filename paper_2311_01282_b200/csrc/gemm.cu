@@ -1574,11 +1574,12 @@ __device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {  // arrives on
 }
 
 template <int BXP, int PER_SM>
-struct PairSmem {  // PER_SM CTAs per SM: a ~192 KB ring, or ~96 KB so two pairs share an SM pair
+struct PairSmem {  // PER_SM CTAs per SM: a ~192 KB ring, or ~96-100 KB so two pairs share an SM pair
     static constexpr uint32_t W_BYTES = 128 * TC_BK * 2;
     static constexpr uint32_t X_BYTES = (BXP / 2) * TC_BK * 2;
     static constexpr uint32_t STAGE_BYTES = W_BYTES + X_BYTES;
-    static constexpr int STAGES = (192 * 1024 / PER_SM) / STAGE_BYTES;
+    static constexpr int RING_KB = PER_SM == 1 ? 192 : (BXP >= 256 ? 96 : 100);
+    static constexpr int STAGES = RING_KB * 1024 / STAGE_BYTES;
     static constexpr uint32_t BAR_OFF = STAGES * STAGE_BYTES;
     static constexpr uint32_t TOTAL = BAR_OFF + (2 * STAGES + 2) * 8 + 16 + 1024;
 };
@@ -1616,7 +1617,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"((uint32_t)BXP)
+                     "r"((uint32_t)(BXP < 32 ? 32 : BXP))
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
@@ -1684,7 +1685,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
     cluster_sync_all();  // the leader's MMAs read both CTAs' smem; TMEM reads done
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)BXP)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)(BXP < 32 ? 32 : BXP))
                      : "memory");
     }
 }
