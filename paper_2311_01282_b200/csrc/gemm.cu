@@ -1587,7 +1587,7 @@ struct PairSmem {  // PER_SM CTAs per SM: a ~192 KB ring, or ~96-100 KB so two p
 template <typename T, int BXP, int PER_SM>
 __global__ void __launch_bounds__(TC_THREADS, PER_SM)
 gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX, T *C,
-                 int64_t ldc, const T *R, int64_t ldr, int M, int N, int K) {
+                 int64_t ldc, const T *R, int64_t ldr, int M, int N, int K, const GemmFuse fz) {
     using S = PairSmem<BXP, PER_SM>;
     constexpr int STAGES = S::STAGES;
     constexpr uint32_t IDESC = umma_idesc_f16(256, BXP, std::is_same<T, __nv_bfloat16>::value);
@@ -1598,6 +1598,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
     uint64_t *empty = full + STAGES;
     uint64_t *tmem_full = empty + STAGES;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 2);
+    __shared__ float s_inv_rms[XF_MAX_M];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const int pair = blockIdx.x >> 1;
@@ -1628,8 +1629,18 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
 
     if (warp == 0) {
         if (lane == 0) {
+            // PDL: the weights depend on no earlier kernel -- the first ring's worth
+            // is requested before the wait, the activations once they are visible
+            const int pre = nkb < STAGES ? nkb : STAGES;
+            for (int i = 0; i < pre; ++i) {
+                if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * S::STAGE_BYTES);
+                tma_load_2d_pair(smem + i * S::STAGE_BYTES, &tmW, &full[i], i * TC_BK, n0, kEvictFirst);
+            }
             pdl_wait();
-            for (int i = 0; i < nkb; ++i) {
+            for (int i = 0; i < pre; ++i)
+                tma_load_2d_pair(smem + i * S::STAGE_BYTES + S::W_BYTES, &tmX, &full[i], i * TC_BK,
+                                 m0 + (int)rank * (BXP / 2), kEvictLast);
+            for (int i = pre; i < nkb; ++i) {
                 const int s = i % STAGES;
                 mbar_wait(&empty[s], ((i / STAGES) & 1) ^ 1);
                 if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
@@ -1661,9 +1672,43 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
         const int quad = warp & 3;
         const int row = quad * 32 + lane;
         const int n = n0 + row;
+        if (fz.x_op == 3) {  // folded RMSNorm: inverse RMS of the token rows, while the MMAs run
+            pdl_wait();
+            inv_rms_rows(s_inv_rms, M, K, fz, threadIdx.x - 64, 128);
+            named_bar_sync(1, 128);
+        }
         mbar_wait(tmem_full, 0);
         tc_fence_after();
         pdl_wait();
+        if (fz.act_out != nullptr) {
+            // SiLU(gate) * up of a tile-interleaved gate|up weight (this CTA's 128
+            // rows = 64 gate rows, then their 64 up rows): rounded values staged in
+            // the idle ring (every MMA has completed), then silu_mul's arithmetic
+            float *rb = reinterpret_cast<float *>(smem);
+#pragma unroll 1
+            for (int c0 = 0; c0 < BXP; c0 += 16) {
+                float v[16];
+                tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + c0, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int m = m0 + c0 + j;
+                    float o = v[j];
+                    if (fz.x_op == 3 && m < M) o *= s_inv_rms[m];
+                    rb[(c0 + j) * 128 + row] = Elem<T>::to_f(Elem<T>::from_f(o));
+                }
+            }
+            named_bar_sync(1, 128);
+            const int tn = n0 >> 7;
+            if (row < 64 && n < N) {
+                for (int c = 0; c < BXP; ++c) {
+                    const int m = m0 + c;
+                    if (m >= M) break;
+                    const float g = rb[c * 128 + row], u = rb[c * 128 + row + 64];
+                    static_cast<T *>(fz.act_out)[(int64_t)m * fz.act_ld + tn * 64 + row] =
+                        Elem<T>::from_f(__fdividef(g, 1.f + __expf(-g)) * u);
+                }
+            }
+        } else {
 #pragma unroll 1
         for (int c0 = 0; c0 < BXP; c0 += 16) {
             float v[16];
@@ -1674,11 +1719,13 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
                     const int m = m0 + c0 + j;
                     if (m < M) {
                         float o = v[j];
+                        if (fz.x_op == 3) o *= s_inv_rms[m];
                         if (R) o += Elem<T>::to_f(R[(int64_t)m * ldr + n]);
                         C[(int64_t)m * ldc + n] = Elem<T>::from_f(o);
                     }
                 }
             }
+        }
         }
     }
     tc_fence_before();
@@ -1691,7 +1738,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
 }
 
 template <typename T, int BXP, int PER_SM>
-static fdpp_status launch_pair(const fdpp_gemm_params *p, cudaStream_t st) {
+static fdpp_status launch_pair(const fdpp_gemm_params *p, cudaStream_t st, const GemmFuse *fz = nullptr) {
     using S = PairSmem<BXP, PER_SM>;
     auto kern = gemm_pair_kernel<T, BXP, PER_SM>;
     static DeviceOnce attr;
@@ -1708,8 +1755,10 @@ static fdpp_status launch_pair(const fdpp_gemm_params *p, cudaStream_t st) {
     if ((s = make_kmajor_map(&mw, p->w, p->N, p->K, p->ldw, 128, p->dtype)) != FDPP_OK) return s;
     if ((s = make_kmajor_map(&mx, p->a, p->M, p->K, p->lda, BXP / 2, p->dtype)) != FDPP_OK) return s;
     const dim3 grid(2 * ceil_div(p->N, 256), ceil_div(p->M, BXP));
+    GemmFuse none;
+    memset(&none, 0, sizeof(none));
     e = launch_kernel_cluster(kern, grid, dim3(TC_THREADS), S::TOTAL, st, 2, mw, mx, static_cast<T *>(p->c),
-                              p->ldc, static_cast<const T *>(p->r), p->ldr, p->M, p->N, p->K);
+                              p->ldc, static_cast<const T *>(p->r), p->ldr, p->M, p->N, p->K, fz ? *fz : none);
     if (e != cudaSuccess) return cuda_status(e, "gemm_pair_kernel launch");
     return FDPP_OK;
 }
@@ -1733,6 +1782,22 @@ static int implc_pair_plan(const fdpp_gemm_params *p) {
     const int pairs = ceil_div(p->N, 256);
     if (mode < 0 && 4 * pairs < sms) return 0;
     return 2 * pairs > sms ? 2 : 1;
+}
+
+// The fused gate|up projection (folded RMSNorm + SiLU.up epilogue) at 33-64
+// tokens runs on CTA pairs: each SM stages half the tokens per weight byte, so
+// the flat tile's M-dependent cost disappears (profiles/r2/flat_gemm_pair_probe.txt)
+// -- when the pairs fill one wave of two per SM pair.  FDPP_PAIR_FUSED=0: off (A/B).
+static bool pair_fused_ok(const fdpp_gemm_params *p, const fdpp_gemm_fuse *f) {
+    static const int mode = [] {
+        const char *e = getenv("FDPP_PAIR_FUSED");
+        return e ? atoi(e) : 1;
+    }();
+    if (!mode || !f || !f->act_out || f->q_out || f->ssq_out || f->ar_world > 1) return false;
+    if (!(f->x_op == 0 || f->x_op == 3) || p->M <= 32 || p->M > 64 || p->ctas != 0 || p->block_x != 0) return false;
+    const int sms = sm_count() > 0 ? sm_count() : 148;
+    const int pairs = ceil_div(p->N, 256);
+    return 2 * pairs > sms && pairs <= sms;
 }
 
 static fdpp_status run_tc(const fdpp_gemm_params *p, bool flat, cudaStream_t st,
@@ -1808,6 +1873,10 @@ static fdpp_status run_tc(const fdpp_gemm_params *p, bool flat, cudaStream_t st,
                 L.fz.ar_ws[r] = static_cast<char *>(fuse->ar_ws[r]);
             }
         }
+    }
+    if (pair_fused_ok(p, fuse)) {  // fused gate|up at 33-64 tokens: the CTA-pair kernel
+        return p->dtype == FDPP_BF16 ? launch_pair<__nv_bfloat16, 64, 2>(p, st, &L.fz)
+                                     : launch_pair<__half, 64, 2>(p, st, &L.fz);
     }
     if ((s = make_kmajor_map(&L.mw, p->w, p->N, p->K, p->ldw, pl.bw, p->dtype)) != FDPP_OK) return s;
     if ((s = make_kmajor_map(&L.mx, p->a, p->M, p->K, p->lda, pl.bx, p->dtype)) != FDPP_OK) return s;

@@ -91,6 +91,31 @@ def test_fused_silu_prologue(torch, mods):
     assert torch.equal(out, ref)        # identical activation bits, identical GEMM path
 
 
+@pytest.mark.parametrize("B", [48, 64])
+def test_fused_rmsnorm_silu_pair(torch, mods, B):
+    """gate|up at 33-64 tokens (folded RMSNorm + SiLU.up) on the CTA-pair kernel
+    (the flat tile's M-dependent cost, profiles/r2/flat_gemm_pair_probe.txt):
+    against an fp32 restatement, output rounded like the unfused buffer."""
+    fd, _lib, gemm, _, D = mods
+    H, F = 4096, 11008
+    g = torch.Generator(device="cuda").manual_seed(B + 1)
+    x = torch.randn((B, H), generator=g, device="cuda").half()
+    w = (torch.randn((2 * F, H), generator=g, device="cuda") / math.sqrt(H)).half()
+    pw = gemm.interleave_gate_up(fd.PackedWeight(w, H, 2 * F))
+    ssq = (x.float() ** 2).sum(1).view(1, B).contiguous()
+    act = torch.empty((B, F), device="cuda", dtype=torch.half)
+    gemm.run_fused(x, pw, x_op=3, ssq_in=ssq, ssq_tiles=1, eps=1e-5, silu_out=act)
+    torch.cuda.synchronize()
+    inv = torch.rsqrt(ssq[0] / H + 1e-5)
+    y = ((x.float() @ w.float().t()) * inv[:, None]).half().float()
+    gate, up = y[:, :F], y[:, F:]
+    ref = (gate / (1 + torch.exp(-gate)) * up).half()
+    assert _rel(act, ref) <= 2e-3
+    act2 = torch.empty_like(act)
+    gemm.run_fused(x, pw, x_op=3, ssq_in=ssq, ssq_tiles=1, eps=1e-5, silu_out=act2)
+    assert torch.equal(act, act2)   # bitwise rerun
+
+
 def test_fused_rope_append_epilogue(torch, mods):
     fd, _lib, gemm, _, D = mods
     B, H, Hq, Hkv, Dh, Lmax = 4, 4096, 32, 32, 128, 40
@@ -206,7 +231,7 @@ def test_fused_silu_epilogue(torch, mods):
     """gate|up GEMM with the SiLU*up epilogue (tile-interleaved weight rows) ==
     the plain fused GEMM into [gate | up] followed by the silu_mul kernel."""
     fd, _lib, gemm, _, D = mods
-    for B, H, F in ((32, 4096, 11008), (5, 1024, 1536)):
+    for B, H, F in ((32, 4096, 11008), (5, 1024, 1536), (64, 4096, 11008)):  # B = 64: the CTA-pair kernel
         g = torch.Generator(device="cuda").manual_seed(B)
         x = torch.randn((B, H), generator=g, device="cuda").half()
         w = (torch.randn((2 * F, H), generator=g, device="cuda") / math.sqrt(H)).half()
