@@ -1794,7 +1794,11 @@ static bool pair_fused_ok(const fdpp_gemm_params *p, const fdpp_gemm_fuse *f) {
         return e ? atoi(e) : 1;
     }();
     if (!mode || !f || !f->act_out || f->q_out || f->ssq_out || f->ar_world > 1) return false;
-    if (!(f->x_op == 0 || f->x_op == 3) || p->M <= 32 || p->M > 64 || p->ctas != 0 || p->block_x != 0) return false;
+    static const int min_m = [] {  // FDPP_PAIR_FUSED_MIN: smallest token count taken (A/B)
+        const char *e = getenv("FDPP_PAIR_FUSED_MIN");
+        return e ? atoi(e) : 33;
+    }();
+    if (!(f->x_op == 0 || f->x_op == 3) || p->M < min_m || p->M > 64 || p->ctas != 0 || p->block_x != 0) return false;
     const int sms = sm_count() > 0 ? sm_count() : 148;
     const int pairs = ceil_div(p->N, 256);
     return 2 * pairs > sms && pairs <= sms;
@@ -1875,6 +1879,9 @@ static fdpp_status run_tc(const fdpp_gemm_params *p, bool flat, cudaStream_t st,
         }
     }
     if (pair_fused_ok(p, fuse)) {  // fused gate|up at 33-64 tokens: the CTA-pair kernel
+        if (p->M <= 32)
+            return p->dtype == FDPP_BF16 ? launch_pair<__nv_bfloat16, 32, 2>(p, st, &L.fz)
+                                         : launch_pair<__half, 32, 2>(p, st, &L.fz);
         return p->dtype == FDPP_BF16 ? launch_pair<__nv_bfloat16, 64, 2>(p, st, &L.fz)
                                      : launch_pair<__half, 64, 2>(p, st, &L.fz);
     }
