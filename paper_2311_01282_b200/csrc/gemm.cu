@@ -1171,29 +1171,38 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             // tile tn is one head: q heads [0, Hq), k heads [Hq, Hq+Hkv), v heads after
             const int i = row & 63;
             const double inv_freq = rope_inv_freq(fz.theta, i, 128);
-            for (int c = c_beg; c < c_end; ++c) {
+            // loop-invariant per thread: which cache / head this tile writes
+            const bool qk = tn < fz.Hq + fz.Hkv;
+            T *base;
+            int64_t tok_stride;
+            if (tn < fz.Hq) {
+                base = static_cast<T *>(fz.q_out) + (int64_t)tn * 128 + row;
+                tok_stride = (int64_t)fz.Hq * 128;
+            } else {
+                base = static_cast<T *>(qk ? fz.k_cache : fz.v_cache) +
+                       (int64_t)(qk ? tn - fz.Hq : tn - fz.Hq - fz.Hkv) * fz.cache_sh + row;
+                tok_stride = fz.cache_sb;
+            }
+            const int64_t cap_rows = fz.cache_sh / 128;
+            const int c_stop = min(c_end, M - m0);  // tokens past M are not stored
+            // four tokens per iteration: their sin/cos and stores are independent chains
+#pragma unroll 4
+            for (int c = c_beg; c < c_stop; ++c) {
                 const int m = m0 + c;
-                if (m >= M) continue;
                 const int p = s_pos[c];
                 const float *xr = rbuf + (c - c_beg) * 128;
-                T *dst;
                 float val;
-                if (tn < fz.Hq + fz.Hkv) {
+                if (qk) {
                     float sn, cs;
                     rope_sincos(p, inv_freq, &sn, &cs);
                     const float x0 = xr[i], x1 = xr[i + 64];
                     val = row < 64 ? x0 * cs - x1 * sn : x1 * cs + x0 * sn;
-                    dst = tn < fz.Hq
-                              ? static_cast<T *>(fz.q_out) + ((int64_t)m * fz.Hq + tn) * 128
-                              : static_cast<T *>(fz.k_cache) + (int64_t)m * fz.cache_sb +
-                                    (int64_t)(tn - fz.Hq) * fz.cache_sh + (int64_t)p * 128;
                 } else {
                     val = xr[row];
-                    dst = static_cast<T *>(fz.v_cache) + (int64_t)m * fz.cache_sb +
-                          (int64_t)(tn - fz.Hq - fz.Hkv) * fz.cache_sh + (int64_t)p * 128;
                 }
+                T *dst = base + (int64_t)m * tok_stride + (tn < fz.Hq ? 0 : (int64_t)p * 128);
                 // capacity guard: cache rows per head = cache_sh / 128
-                if (tn < fz.Hq || (p >= 0 && (int64_t)p < fz.cache_sh / 128)) dst[row] = Elem<T>::from_f(val);
+                if (tn < fz.Hq || (p >= 0 && (int64_t)p < cap_rows)) *dst = Elem<T>::from_f(val);
             }
         }
     }
