@@ -1150,15 +1150,17 @@ gemm_cluster_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_consta
             cl_allreduce<T, MMA_N>(ep, fz, slice, epoch, threadIdx.x - 64);
         }
         if (fz.ssq_out || rope || silu) named_bar_sync(1, 128);
-        if (silu && row < 64) {
+        if (silu) {
             // tile tn = gate rows [64 tn, 64 tn + 64) then the matching up rows; values
-            // staged rounded like the unfused gate|up buffer, then silu_mul's arithmetic
-            for (int c = c_beg; c < c_end; ++c) {
-                const int m = m0 + c;
-                if (m >= M) continue;
-                const float g = rbuf[(c - c_beg) * 128 + row], u = rbuf[(c - c_beg) * 128 + row + 64];
-                static_cast<T *>(fz.act_out)[(int64_t)m * fz.act_ld + tn * 64 + row] =
-                    Elem<T>::from_f(__fdividef(g, 1.f + __expf(-g)) * u);
+            // staged rounded like the unfused gate|up buffer, then silu_mul's arithmetic.
+            // All 128 threads: thread (r, half) takes gate row r for every other token.
+            const int r = row & 63, half = row >> 6;
+            const int c_stop = min(c_end, M - m0);
+            T *dst = static_cast<T *>(fz.act_out) + tn * 64 + r;
+#pragma unroll 4
+            for (int c = c_beg + half; c < c_stop; c += 2) {
+                const float g = rbuf[(c - c_beg) * 128 + r], u = rbuf[(c - c_beg) * 128 + r + 64];
+                dst[(int64_t)(m0 + c) * fz.act_ld] = Elem<T>::from_f(__fdividef(g, 1.f + __expf(-g)) * u);
             }
         }
         if (fz.ssq_out && row < c_end - c_beg) {
