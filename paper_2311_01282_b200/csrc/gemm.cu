@@ -1709,14 +1709,15 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant_
                 }
             }
             named_bar_sync(1, 128);
-            const int tn = n0 >> 7;
-            if (row < 64 && n < N) {
-                for (int c = 0; c < BXP; ++c) {
-                    const int m = m0 + c;
-                    if (m >= M) break;
-                    const float g = rb[c * 128 + row], u = rb[c * 128 + row + 64];
-                    static_cast<T *>(fz.act_out)[(int64_t)m * fz.act_ld + tn * 64 + row] =
-                        Elem<T>::from_f(__fdividef(g, 1.f + __expf(-g)) * u);
+            // all 128 threads: thread (r, half) takes gate row r for every other token
+            const int tn = n0 >> 7, r = row & 63, half = row >> 6;
+            if (n0 + r < N) {
+                const int c_stop = min(BXP, M - m0);
+                T *dst = static_cast<T *>(fz.act_out) + tn * 64 + r;
+#pragma unroll 4
+                for (int c = half; c < c_stop; c += 2) {
+                    const float g = rb[c * 128 + r], u = rb[c * 128 + r + 64];
+                    dst[(int64_t)(m0 + c) * fz.act_ld] = Elem<T>::from_f(__fdividef(g, 1.f + __expf(-g)) * u);
                 }
             }
         } else {

@@ -6,7 +6,7 @@ for i in 1 2; do
   true FDPP_LIB=$PWD/tools/ab_old/libfdpp.so timeout 300 python tools/qkv_epi_probe.py | sed 's/^/old /'
   true timeout 300 python tools/qkv_epi_probe.py | sed 's/^/new /'
 done
-for i in 1 2; do for b in 32 64 8; do
+for i in 1 2 3; do for b in ${AB_BATCHES:-32 64 8}; do
   FDPP_LIB=$PWD/tools/ab_old/libfdpp.so timeout 300 python bench.py --no-cpu --no-extras --steps 50 --batch $b > /tmp/o.json 2>/dev/null; show "old B$b" /tmp/o.json
   timeout 300 python bench.py --no-cpu --no-extras --steps 50 --batch $b > /tmp/n.json 2>/dev/null; show "new B$b" /tmp/n.json
 done; done
